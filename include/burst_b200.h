@@ -1,0 +1,141 @@
+/* burst_b200.h -- C ABI of the B200-native BurstAttention hot path.
+ *
+ * Every entry point is asynchronous on the caller's CUDA stream (passed as an
+ * opaque `void*` cudaStream_t), takes plain device pointers and sizes, never
+ * allocates, and returns 0 or a BURST_E_* code (message via burst_last_error).
+ * The error codes mirror the reference taxonomy (pkg/src/burstsim/errors.py:4-33).
+ *
+ * Reference interfaces replaced (all /root/reference/pkg/src/burstsim/):
+ *   burst_lao_fwd        local_attn.local_forward_tiled   (local_attn.py:207-248)
+ *                        + PartialAttn.merge               (local_attn.py:101-120)
+ *                        = ring.forward_step hop merge     (ring.py:158-181)
+ *   burst_fwd_finalize   PartialAttn.finalize / ring.finalize_forward
+ *                                                          (local_attn.py:127-135, ring.py:184-188)
+ *   burst_bwd_preprocess ring.init_backward D = rowsum(dO*O) (ring.py:195-218)
+ *   burst_lao_bwd        local_attn.local_backward         (local_attn.py:255-289)
+ *                        = ring.backward_step accumulation (ring.py:221-242)
+ *   burst_bwd_finalize   sim._collect gradient assembly    (sim.py:450-471)
+ *   burst_ring_*         sim.RingChannel send/recv, DoubleBuffer (sim.py:281-332)
+ *
+ * Tensor layouts (row-major, contiguous):
+ *   q, k, v, o, dout, dq, dk, dv : [batch, n, heads, head_dim]  (bf16 or f32)
+ *   lse, m, l                    : [batch, heads, n] f32 (lse natural log, m log2 units)
+ *   o_acc, dq_acc, dk/dv partials: f32 "TL" workspace, burst_workspace_floats()
+ *                                  elements, layout [B*H][ceil(n/128)][D/4][128][4]
+ */
+#ifndef BURST_B200_H
+#define BURST_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define BURST_API __attribute__((visibility("default")))
+#else
+#define BURST_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  BURST_OK = 0,
+  BURST_E_SHAPE = 1,      /* ShapeError */
+  BURST_E_MASK = 2,       /* MaskError: a query row saw no key */
+  BURST_E_NONFINITE = 3,  /* NonFiniteError */
+  BURST_E_ORDER = 4,      /* MissingForwardError */
+  BURST_E_CUDA = 5,
+  BURST_E_NCCL = 6,
+  BURST_E_DEADLOCK = 7,   /* DeadlockError */
+  BURST_E_UNSUPPORTED = 8
+};
+
+enum { BURST_DTYPE_BF16 = 0, BURST_DTYPE_F32 = 1 };
+
+/* Global position of local row i: i < seg_len ? pos0 + i : pos1 + (i - seg_len).
+ * Monotone (pos0 + seg_len <= pos1).  Contiguous shards use one segment
+ * (seg_len >= n); zigzag shards hold chunks r and 2G-1-r. */
+typedef struct {
+  int64_t pos0, pos1, seg_len;
+} burst_posmap;
+
+/* One hop: the pinned query block (n_q rows) against a visiting key/value block
+ * (n_k rows).  Only query rows [q_begin, q_begin+q_len) and key rows
+ * [k_begin, k_begin+k_len) participate (zigzag hop classes).  With `causal`,
+ * key j is visible to query i iff k_map(j) <= q_map(i) (masking.py:116-117). */
+typedef struct {
+  int32_t batch, heads, head_dim, dtype;
+  int64_t n_q, n_k;
+  int64_t q_begin, q_len, k_begin, k_len;
+  float softmax_scale;
+  int32_t causal;
+  burst_posmap q_map, k_map;
+} burst_hop;
+
+/* Elements (float) of one TL workspace for [batch, n, heads, head_dim]. */
+BURST_API size_t burst_workspace_floats(int batch, int heads, int head_dim, int64_t n);
+
+/* LAO forward of one hop fused with the GAO merge into the running state
+ * (o_acc TL, m/l in log2 units).  first_hop: ignore the incoming state.
+ * finalize: normalise and write o_out (dtype) and lse_out instead of the state. */
+BURST_API int burst_lao_fwd(const burst_hop* hop, const void* q, const void* k, const void* v, float* o_acc,
+                  float* m, float* l, void* o_out, float* lse_out, int first_hop, int finalize,
+                  void* stream);
+
+/* Normalise a running state: o_out = o_acc / l, lse = ln-domain(m, l). */
+BURST_API int burst_fwd_finalize(int dtype, int batch, int heads, int head_dim, int64_t n,
+                       const float* o_acc, const float* m, const float* l, void* o_out,
+                       float* lse_out, void* stream);
+
+/* Backward stats for every (b, h, row) of a [batch, n] query block, packed as
+ * stats[0][B*H][ceil(n/128)*128] = lse * log2(e) and stats[1][...] = D =
+ * rowsum(dout * o) (padded rows: +inf / 0); also zeroes dq_acc (TL) if given.
+ * `stats` holds 2 * batch * heads * ceil(n/128) * 128 floats. */
+BURST_API int burst_bwd_preprocess(int dtype, int batch, int heads, int head_dim, int64_t n, const void* o,
+                         const void* dout, const float* lse, float* stats, float* dq_acc,
+                         void* stream);
+
+/* LAO backward of one hop: dq_acc += scale dS K (TL over n_q, fp32 atomics for
+ * bf16); the visiting block's dK/dV contributions (TL over n_k) are written to
+ * dk_acc/dv_acc, or added to them when accumulate != 0.  `stats` comes from
+ * burst_bwd_preprocess on the pinned query block. */
+BURST_API int burst_lao_bwd(const burst_hop* hop, const void* q, const void* k, const void* v,
+                  const void* dout, const float* stats, float* dq_acc, float* dk_acc,
+                  float* dv_acc, int accumulate, void* stream);
+
+/* dq = dq_acc; dk = sum of nparts dk partials; dv likewise (TL f32 -> dtype). */
+BURST_API int burst_bwd_finalize(int dtype, int batch, int heads, int head_dim, int64_t n,
+                       const float* dq_acc, const float* const* dk_parts,
+                       const float* const* dv_parts, int nparts, void* dq, void* dk, void* dv,
+                       void* stream);
+
+/* Non-zero device-side flags raised by kernels since the last call (bit 0: a
+ * row with no visible key, bit 1: non-finite output).  Synchronises `stream`. */
+BURST_API int burst_read_flags(void* stream, int* flags_out);
+
+/* Ring transport over NCCL (libnccl.so.2 resolved at run time). */
+BURST_API int burst_ring_unique_id(void* out_128_bytes);
+BURST_API int burst_ring_create(const void* unique_id_128_bytes, int rank, int world, int device,
+                      void** ring);
+/* Grouped send(send_to) + recv(recv_from) of `bytes` on `stream`. */
+BURST_API int burst_ring_exchange(void* ring, const void* send, void* recv, size_t bytes, int send_to,
+                        int recv_from, void* stream);
+/* One grouped exchange of several sends/receives (K/V rotation plus the dK/dV
+ * contribution sent to its home rank) on `stream`. */
+typedef struct {
+  void* buf;
+  size_t bytes;
+  int32_t peer;
+  int32_t is_send;
+} burst_p2p;
+BURST_API int burst_ring_sendrecv(void* ring, const burst_p2p* ops, int nops, void* stream);
+BURST_API int burst_ring_destroy(void* ring);
+
+BURST_API const char* burst_last_error(void);
+BURST_API int burst_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BURST_B200_H */

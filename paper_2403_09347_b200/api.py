@@ -1,0 +1,141 @@
+"""Public entry points.
+
+`burst_attn_func(q, k, v, causal, softmax_scale, group)` is the drop-in
+attention call of the north star: q/k/v are this rank's sequence shards
+[batch, n_local, heads, head_dim]; it returns (out, lse) and is differentiable
+(autograd backward = the ring backward).  It replaces the reference's pass-level
+run_ring_pass forward+backward (sim.py:501-657) for one rank.
+
+`run_ring_pass` / `burst_attn_global` run a whole G-device ring inside one
+process on one GPU (loopback transport, one thread per simulated device) and
+mirror the reference's pass-level API for parity tests.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from .errors import ConfigError, ShapeError
+from .kernels import CudaKernels, check_qkv, default_scale
+from .ring import NcclTransport, SoloTransport, ring_backward, ring_forward, run_ranks
+from .schedule import shard, unshard
+
+_kernels = None
+_transports = {}
+
+
+def _default_kernels():
+    global _kernels
+    if _kernels is None:
+        _kernels = CudaKernels()
+    return _kernels
+
+
+def _transport_for(group):
+    import torch.distributed as dist
+    if group is None and not (dist.is_available() and dist.is_initialized()):
+        return SoloTransport()
+    world = dist.get_world_size(group)
+    if world == 1:
+        return SoloTransport()
+    key = (id(group), torch.cuda.current_device())
+    if key not in _transports:
+        _transports[key] = NcclTransport(group)
+    return _transports[key]
+
+
+class _BurstAttnFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, q, k, v, scale, causal, zigzag, transport, kernels):
+        o, lse = ring_forward(q, k, v, scale, causal, zigzag, transport, kernels)
+        ctx.save_for_backward(q, k, v, o, lse)
+        ctx.cfg = (scale, causal, zigzag, transport, kernels)
+        ctx.mark_non_differentiable(lse)
+        return o, lse
+
+    @staticmethod
+    def backward(ctx, do, _dlse):
+        q, k, v, o, lse = ctx.saved_tensors
+        scale, causal, zigzag, transport, kernels = ctx.cfg
+        dq, dk, dv = ring_backward(q, k, v, o, lse, do.contiguous(), scale, causal, zigzag,
+                                   transport, kernels)
+        return dq, dk, dv, None, None, None, None, None
+
+
+def burst_attn_func(q, k, v, causal: bool = False, softmax_scale: float | None = None,
+                    group=None, zigzag: bool | None = None, *, _transport=None, _kernels=None):
+    """BurstAttention over the ranks of `group` (NCCL ring over NVLink).
+
+    q, k, v: [batch, n_local, heads, head_dim] shards of the global sequence
+    (contiguous blocks, or zigzag chunks {rank, 2G-1-rank} when causal and
+    zigzag -- the default for causal with G > 1; see `schedule.shard`).
+    Returns (out [batch, n_local, heads, head_dim], lse [batch, heads, n_local]).
+    """
+    check_qkv(q, k, v) if _kernels is None else None
+    if q.shape[1] != k.shape[1]:
+        raise ShapeError("ring shards must have equal query and key lengths")
+    scale = default_scale(q.shape[-1]) if softmax_scale is None else float(softmax_scale)
+    if not scale > 0:
+        raise ShapeError(f"scale must be finite and positive, got {scale}")
+    transport = _transport if _transport is not None else _transport_for(group)
+    kernels = _kernels if _kernels is not None else _default_kernels()
+    if zigzag is None:
+        zigzag = bool(causal) and transport.world > 1
+    if zigzag and q.shape[1] % 2:
+        raise ShapeError("zigzag shards need an even local length")
+    return _BurstAttnFn.apply(q, k, v, scale, bool(causal), bool(zigzag), transport, kernels)
+
+
+@dataclass
+class PassResult:
+    """Mirror of sim.PassResult (sim.py:386-397): outputs and grads, global order."""
+    out: torch.Tensor
+    lse: torch.Tensor
+    dq: torch.Tensor | None = None
+    dk: torch.Tensor | None = None
+    dv: torch.Tensor | None = None
+
+
+def run_ring_pass(q, k, v, world: int, causal: bool = False, softmax_scale: float | None = None,
+                  dout=None, zigzag: bool | None = None, kernels=None) -> PassResult:
+    """Whole-ring forward (+ backward when `dout` is given) of GLOBAL tensors
+    [batch, N, heads, head_dim] over `world` simulated devices on this GPU.
+
+    Mirrors build_cluster + run_ring_pass (sim.py:366-383, 501-657) with the
+    threaded executor: one thread per device, real CUDA kernels, device
+    copies for the ring hand-off.
+    """
+    if world < 1:
+        raise ConfigError(f"gpus must be a positive integer, got {world}")
+    kernels = kernels if kernels is not None else _default_kernels()
+    if kernels.name == "cuda":
+        check_qkv(q, k, v)
+    if zigzag is None:
+        zigzag = bool(causal) and world > 1
+    N = q.shape[1]
+    if N % (2 * world if zigzag else world):
+        raise ConfigError(f"gpus={world} does not divide seq={N}" + (" into 2G chunks" if zigzag else ""))
+    scale = default_scale(q.shape[-1]) if softmax_scale is None else float(softmax_scale)
+    shards = [[shard(t, r, world, zigzag) for r in range(world)] for t in (q, k, v)]
+    do_sh = [shard(dout, r, world, zigzag) for r in range(world)] if dout is not None else None
+
+    def one(rank, transport):
+        qs, ks, vs = shards[0][rank], shards[1][rank], shards[2][rank]
+        o, lse = ring_forward(qs, ks, vs, scale, causal, zigzag, transport, kernels)
+        if do_sh is None:
+            return o, lse, None
+        g = ring_backward(qs, ks, vs, o, lse, do_sh[rank], scale, causal, zigzag, transport,
+                          kernels)
+        return o, lse, g
+
+    res = run_ranks(world, one)
+    out = unshard([x[0] for x in res], zigzag, dim=1)
+    lse = unshard([x[1] for x in res], zigzag, dim=2)
+    if dout is None:
+        return PassResult(out, lse)
+    dq = unshard([x[2][0] for x in res], zigzag, dim=1)
+    dk = unshard([x[2][1] for x in res], zigzag, dim=1)
+    dv = unshard([x[2][2] for x in res], zigzag, dim=1)
+    return PassResult(out, lse, dq, dk, dv)

@@ -1,0 +1,351 @@
+// C ABI (include/burst_b200.h): argument validation, TMA tensor maps, launch
+// configuration, error mapping onto the reference taxonomy (errors.py:4-33).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/burst_b200.h"
+#include "aux_kernels.cuh"
+#include "lao_bwd_sm100.cuh"
+#include "lao_fwd_sm100.cuh"
+#include "simt_f32.cuh"
+
+using namespace burst;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(x)                                                                  \
+  do {                                                                               \
+    cudaError_t e_ = (x);                                                            \
+    if (e_ != cudaSuccess) return fail(BURST_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define CHECK_LAUNCH()                                                               \
+  do {                                                                               \
+    cudaError_t e_ = cudaGetLastError();                                             \
+    if (e_ != cudaSuccess) return fail(BURST_E_CUDA, std::string("launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 4-D map over a [B, n, H, D] bf16 tensor; box = 64 columns x 1 head x 128 rows.
+int make_tmap(CUtensorMap* tm, const void* base, int64_t n, int H, int D, int B) {
+  auto fn = encode_fn();
+  if (!fn) return fail(BURST_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0)
+    return fail(BURST_E_SHAPE, "tensor base must be 16-byte aligned");
+  cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)H, (cuuint64_t)n, (cuuint64_t)B};
+  cuuint64_t strides[3] = {(cuuint64_t)D * 2, (cuuint64_t)H * D * 2, (cuuint64_t)n * H * D * 2};
+  cuuint32_t box[4] = {64, 1, 128, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(BURST_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return BURST_OK;
+}
+
+int* device_flags() {
+  static int* flags[64] = {nullptr};
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (!flags[dev]) {
+    if (cudaMalloc(&flags[dev], sizeof(int)) != cudaSuccess) return nullptr;
+    cudaMemset(flags[dev], 0, sizeof(int));
+  }
+  return flags[dev];
+}
+
+bool valid_map(const burst_posmap& m) { return m.seg_len >= 0 && m.pos0 + m.seg_len <= m.pos1; }
+
+int check_hop(const burst_hop* h) {
+  if (!h) return fail(BURST_E_SHAPE, "hop descriptor is null");
+  if (h->batch < 1 || h->heads < 1) return fail(BURST_E_SHAPE, "batch and heads must be positive");
+  if (h->n_q < 0 || h->n_k < 0 || h->q_begin < 0 || h->k_begin < 0 || h->q_len < 0 || h->k_len < 0 ||
+      h->q_begin + h->q_len > h->n_q || h->k_begin + h->k_len > h->n_k)
+    return fail(BURST_E_SHAPE, "hop row ranges exceed the q/k extents");
+  if (!(h->softmax_scale > 0.f)) return fail(BURST_E_SHAPE, "softmax_scale must be finite and positive");
+  if (h->n_q > INT32_MAX || h->n_k > INT32_MAX) return fail(BURST_E_SHAPE, "sequence too long for TMA coordinates");
+  if (h->causal && (!valid_map(h->q_map) || !valid_map(h->k_map)))
+    return fail(BURST_E_SHAPE, "position maps must be monotone (pos0 + seg_len <= pos1)");
+  if (h->dtype == BURST_DTYPE_BF16) {
+    if (h->head_dim != 64 && h->head_dim != 128)
+      return fail(BURST_E_UNSUPPORTED, "bf16 path supports head_dim 64 or 128");
+    if ((h->q_begin % 8) || (h->k_begin % 8))
+      return fail(BURST_E_SHAPE, "bf16 path needs q_begin/k_begin multiples of 8");
+  } else if (h->dtype == BURST_DTYPE_F32) {
+    if (h->head_dim != 16 && h->head_dim != 32 && h->head_dim != 64)
+      return fail(BURST_E_UNSUPPORTED, "f32 path supports head_dim 16, 32 or 64");
+  } else {
+    return fail(BURST_E_UNSUPPORTED, "dtype must be BURST_DTYPE_BF16 or BURST_DTYPE_F32");
+  }
+  return BURST_OK;
+}
+
+template <typename K>
+int set_smem(K kernel, int bytes) {
+  CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  return BURST_OK;
+}
+
+int grid_for(int64_t work, int block) {
+  int64_t g = (work + block - 1) / block;
+  if (g > 148 * 32) g = 148 * 32;
+  return (int)(g < 1 ? 1 : g);
+}
+
+template <int D>
+int launch_fwd_bf16(const burst_hop* h, const void* q, const void* k, const void* v, float* o_acc,
+                    float* m, float* l, void* o_out, float* lse, int first, int fin, cudaStream_t st) {
+  fwd::Params p;
+  memset(&p, 0, sizeof(p));
+  int rc;
+  if ((rc = make_tmap(&p.tm_q, q, h->n_q, h->heads, D, h->batch))) return rc;
+  if ((rc = make_tmap(&p.tm_k, k, h->n_k, h->heads, D, h->batch))) return rc;
+  if ((rc = make_tmap(&p.tm_v, v, h->n_k, h->heads, D, h->batch))) return rc;
+  p.o_acc = o_acc; p.m_run = m; p.l_run = l; p.o_out = o_out; p.lse_out = lse;
+  p.flags = device_flags();
+  p.hop = *h;
+  p.scale_log2 = h->softmax_scale * kLog2e;
+  p.first_hop = first; p.finalize = fin;
+  static std::once_flag once;
+  static int attr_rc = 0;
+  std::call_once(once, [] { attr_rc = set_smem(fwd::lao_fwd_kernel<D>, fwd::Cfg<D>::kSmemBytes); });
+  if (attr_rc) return attr_rc;
+  dim3 grid((unsigned)ceil_div(h->q_len, 2 * fwd::BM), h->heads, h->batch);
+  fwd::lao_fwd_kernel<D><<<grid, fwd::kThreads, fwd::Cfg<D>::kSmemBytes, st>>>(p);
+  CHECK_LAUNCH();
+  return BURST_OK;
+}
+
+template <int D>
+int launch_fwd_f32(const burst_hop* h, const void* q, const void* k, const void* v, float* o_acc,
+                   float* m, float* l, void* o_out, float* lse, int first, int fin, cudaStream_t st) {
+  simt::FwdParams p;
+  p.q = (const float*)q; p.k = (const float*)k; p.v = (const float*)v;
+  p.o_acc = o_acc; p.m_run = m; p.l_run = l; p.o_out = (float*)o_out; p.lse_out = lse;
+  p.flags = device_flags();
+  p.hop = *h;
+  p.scale_log2 = h->softmax_scale * kLog2e;
+  p.first_hop = first; p.finalize = fin;
+  dim3 grid((unsigned)ceil_div(h->q_len, simt::kRows), h->heads, h->batch);
+  simt::simt_fwd_kernel<D><<<grid, simt::kRows, 0, st>>>(p);
+  CHECK_LAUNCH();
+  return BURST_OK;
+}
+
+template <int D>
+int launch_bwd_bf16(const burst_hop* h, const void* q, const void* k, const void* v, const void* dout,
+                    const float* stats, float* dq_acc, float* dk, float* dv, int acc, cudaStream_t st) {
+  bwd::Params p;
+  memset(&p, 0, sizeof(p));
+  int rc;
+  if ((rc = make_tmap(&p.tm_q, q, h->n_q, h->heads, D, h->batch))) return rc;
+  if ((rc = make_tmap(&p.tm_do, dout, h->n_q, h->heads, D, h->batch))) return rc;
+  if ((rc = make_tmap(&p.tm_k, k, h->n_k, h->heads, D, h->batch))) return rc;
+  if ((rc = make_tmap(&p.tm_v, v, h->n_k, h->heads, D, h->batch))) return rc;
+  p.stats = stats; p.dq_acc = dq_acc; p.dk_acc = dk; p.dv_acc = dv;
+  p.hop = *h;
+  p.scale_log2 = h->softmax_scale * kLog2e;
+  p.scale = h->softmax_scale;
+  p.accumulate = acc;
+  static std::once_flag once;
+  static int attr_rc = 0;
+  std::call_once(once, [] { attr_rc = set_smem(bwd::lao_bwd_kernel<D>, bwd::Cfg<D>::kSmemBytes); });
+  if (attr_rc) return attr_rc;
+  dim3 grid((unsigned)ceil_div(h->k_len, bwd::BN), h->heads, h->batch);
+  bwd::lao_bwd_kernel<D><<<grid, bwd::kThreads, bwd::Cfg<D>::kSmemBytes, st>>>(p);
+  CHECK_LAUNCH();
+  return BURST_OK;
+}
+
+template <int D>
+int launch_bwd_f32(const burst_hop* h, const void* q, const void* k, const void* v, const void* dout,
+                   const float* stats, float* dq_acc, float* dk, float* dv, int acc, cudaStream_t st) {
+  simt::BwdParams p;
+  p.q = (const float*)q; p.k = (const float*)k; p.v = (const float*)v; p.dout = (const float*)dout;
+  p.stats = stats; p.dq_acc = dq_acc; p.dk_acc = dk; p.dv_acc = dv;
+  p.hop = *h;
+  p.scale_log2 = h->softmax_scale * kLog2e;
+  p.scale = h->softmax_scale;
+  p.accumulate = acc;
+  const int smem = 2 * simt::kRows * (D + 1) * 4;
+  static std::once_flag once;
+  static int attr_rc = 0;
+  std::call_once(once, [smem] { attr_rc = set_smem(simt::simt_bwd_dkv_kernel<D>, smem); });
+  if (attr_rc) return attr_rc;
+  if (h->q_len > 0) {
+    dim3 g1((unsigned)ceil_div(h->q_len, simt::kRows), h->heads, h->batch);
+    simt::simt_bwd_dq_kernel<D><<<g1, simt::kRows, 0, st>>>(p);
+    CHECK_LAUNCH();
+  }
+  dim3 g2((unsigned)ceil_div(h->k_len, simt::kRows), h->heads, h->batch);
+  simt::simt_bwd_dkv_kernel<D><<<g2, simt::kRows, smem, st>>>(p);
+  CHECK_LAUNCH();
+  return BURST_OK;
+}
+
+int check_dims(int dtype, int B, int H, int D, int64_t n) {
+  if (B < 1 || H < 1 || n < 0) return fail(BURST_E_SHAPE, "batch/heads must be positive, n >= 0");
+  if (dtype == BURST_DTYPE_BF16 && D != 64 && D != 128)
+    return fail(BURST_E_UNSUPPORTED, "bf16 path supports head_dim 64 or 128");
+  if (dtype == BURST_DTYPE_F32 && D != 16 && D != 32 && D != 64)
+    return fail(BURST_E_UNSUPPORTED, "f32 path supports head_dim 16, 32 or 64");
+  if (dtype != BURST_DTYPE_BF16 && dtype != BURST_DTYPE_F32) return fail(BURST_E_UNSUPPORTED, "bad dtype");
+  return BURST_OK;
+}
+
+}  // namespace
+
+int burst_internal_fail(int code, const std::string& msg) { return fail(code, msg); }
+
+extern "C" {
+
+int burst_version(void) { return 1; }
+
+const char* burst_last_error(void) { return g_err.c_str(); }
+
+size_t burst_workspace_floats(int batch, int heads, int head_dim, int64_t n) {
+  return (size_t)batch * heads * (size_t)ceil_div(n, 128) * 128 * head_dim;
+}
+
+int burst_lao_fwd(const burst_hop* hop, const void* q, const void* k, const void* v, float* o_acc,
+                  float* m, float* l, void* o_out, float* lse_out, int first_hop, int finalize,
+                  void* stream) {
+  int rc = check_hop(hop);
+  if (rc) return rc;
+  if (!finalize && (!o_acc || !m || !l)) return fail(BURST_E_SHAPE, "running state pointers are null");
+  if (finalize && (!o_out || !lse_out)) return fail(BURST_E_SHAPE, "output pointers are null");
+  if (!first_hop && (!o_acc || !m || !l))
+    return fail(BURST_E_ORDER, "non-first hop needs the running state (init_forward first)");
+  if (hop->q_len == 0) return BURST_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (hop->dtype == BURST_DTYPE_BF16) {
+    if (hop->head_dim == 128) return launch_fwd_bf16<128>(hop, q, k, v, o_acc, m, l, o_out, lse_out, first_hop, finalize, st);
+    return launch_fwd_bf16<64>(hop, q, k, v, o_acc, m, l, o_out, lse_out, first_hop, finalize, st);
+  }
+  switch (hop->head_dim) {
+    case 16: return launch_fwd_f32<16>(hop, q, k, v, o_acc, m, l, o_out, lse_out, first_hop, finalize, st);
+    case 32: return launch_fwd_f32<32>(hop, q, k, v, o_acc, m, l, o_out, lse_out, first_hop, finalize, st);
+    default: return launch_fwd_f32<64>(hop, q, k, v, o_acc, m, l, o_out, lse_out, first_hop, finalize, st);
+  }
+}
+
+int burst_fwd_finalize(int dtype, int batch, int heads, int head_dim, int64_t n, const float* o_acc,
+                       const float* m, const float* l, void* o_out, float* lse_out, void* stream) {
+  int rc = check_dims(dtype, batch, heads, head_dim, n);
+  if (rc) return rc;
+  if (n == 0) return BURST_OK;
+  const int64_t work = (int64_t)burst_workspace_floats(batch, heads, head_dim, n) / 4;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == BURST_DTYPE_BF16)
+    aux::finalize_kernel<__nv_bfloat16><<<grid_for(work, 256), 256, 0, st>>>(
+        batch, heads, head_dim, n, o_acc, m, l, (__nv_bfloat16*)o_out, lse_out, device_flags());
+  else
+    aux::finalize_kernel<float><<<grid_for(work, 256), 256, 0, st>>>(
+        batch, heads, head_dim, n, o_acc, m, l, (float*)o_out, lse_out, device_flags());
+  CHECK_LAUNCH();
+  return BURST_OK;
+}
+
+int burst_bwd_preprocess(int dtype, int batch, int heads, int head_dim, int64_t n, const void* o,
+                         const void* dout, const float* lse, float* stats, float* dq_acc, void* stream) {
+  int rc = check_dims(dtype, batch, heads, head_dim, n);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t ws = burst_workspace_floats(batch, heads, head_dim, n);
+  if (dq_acc) CUDA_TRY(cudaMemsetAsync(dq_acc, 0, ws * sizeof(float), st));
+  if (n == 0) return BURST_OK;
+  const int64_t rows = (int64_t)batch * heads * ceil_div(n, 128) * 128;
+  if (dtype == BURST_DTYPE_BF16)
+    aux::preprocess_kernel<__nv_bfloat16><<<grid_for(rows * 32, 256), 256, 0, st>>>(
+        batch, heads, head_dim, n, (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, lse, stats);
+  else
+    aux::preprocess_kernel<float><<<grid_for(rows * 32, 256), 256, 0, st>>>(
+        batch, heads, head_dim, n, (const float*)o, (const float*)dout, lse, stats);
+  CHECK_LAUNCH();
+  return BURST_OK;
+}
+
+int burst_lao_bwd(const burst_hop* hop, const void* q, const void* k, const void* v, const void* dout,
+                  const float* stats, float* dq_acc, float* dk_acc, float* dv_acc, int accumulate,
+                  void* stream) {
+  int rc = check_hop(hop);
+  if (rc) return rc;
+  if (!stats) return fail(BURST_E_ORDER, "backward needs the preprocess stats (forward lse, D)");
+  if (hop->k_len == 0) return BURST_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (hop->dtype == BURST_DTYPE_BF16) {
+    if (hop->head_dim == 128) return launch_bwd_bf16<128>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
+    return launch_bwd_bf16<64>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
+  }
+  switch (hop->head_dim) {
+    case 16: return launch_bwd_f32<16>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
+    case 32: return launch_bwd_f32<32>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
+    default: return launch_bwd_f32<64>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
+  }
+}
+
+int burst_bwd_finalize(int dtype, int batch, int heads, int head_dim, int64_t n, const float* dq_acc,
+                       const float* const* dk_parts, const float* const* dv_parts, int nparts, void* dq,
+                       void* dk, void* dv, void* stream) {
+  int rc = check_dims(dtype, batch, heads, head_dim, n);
+  if (rc) return rc;
+  if (nparts < 0 || nparts > 16) return fail(BURST_E_SHAPE, "nparts must be in [0, 16]");
+  if (n == 0) return BURST_OK;
+  aux::Parts pk, pv;
+  for (int i = 0; i < 16; ++i) {
+    pk.p[i] = i < nparts ? dk_parts[i] : nullptr;
+    pv.p[i] = i < nparts ? dv_parts[i] : nullptr;
+  }
+  const int64_t work = (int64_t)burst_workspace_floats(batch, heads, head_dim, n) / 4;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == BURST_DTYPE_BF16)
+    aux::bwd_finalize_kernel<__nv_bfloat16><<<grid_for(work, 256), 256, 0, st>>>(
+        batch, heads, head_dim, n, dq_acc, pk, pv, nparts, dq_acc ? (__nv_bfloat16*)dq : nullptr,
+        (__nv_bfloat16*)dk, (__nv_bfloat16*)dv);
+  else
+    aux::bwd_finalize_kernel<float><<<grid_for(work, 256), 256, 0, st>>>(
+        batch, heads, head_dim, n, dq_acc, pk, pv, nparts, dq_acc ? (float*)dq : nullptr, (float*)dk,
+        (float*)dv);
+  CHECK_LAUNCH();
+  return BURST_OK;
+}
+
+int burst_read_flags(void* stream, int* flags_out) {
+  int* f = device_flags();
+  if (!f) return fail(BURST_E_CUDA, "flag buffer allocation failed");
+  int h = 0;
+  CUDA_TRY(cudaMemcpyAsync(&h, f, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+  CUDA_TRY(cudaMemsetAsync(f, 0, sizeof(int), (cudaStream_t)stream));
+  if (flags_out) *flags_out = h;
+  return BURST_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,379 @@
+// LAO backward on sm_100a, K/V-stationary.
+//
+// Reference semantics: one call = ring.backward_step (ring.py:221-242) for every
+// (batch, head) slice, i.e. local_backward (local_attn.py:255-289, tiled form
+// _backward_tiled 313-353) over the hop's rectangle:
+//     P = exp(S - lse); dV += P^T dO; dP = dO V^T; dS = P * (dP - D);
+//     dQ += scale dS K;  dK += scale dS^T Q
+// computed transposed per key tile (S^T = K Q^T), so the visiting block's dK/dV
+// accumulate in TMEM across all query tiles and dQ (pinned on this rank) is
+// reduced into an fp32 workspace with vector atomics.
+//
+// CTA = one key tile of 128 rows (K, V stationary in SMEM); loops over the
+// hop's query tiles of 128 (Q_i, dO_i, lse_i, D_i double-buffered by TMA).
+//   warps 0-3  P / dS warpgroup (thread = key row = TMEM lane); dK/dV epilogue
+//   warps 4-7  dQ drain warpgroup (thread = query row of the dQ tile)
+//   warp  8    TMA producer (+ TMEM allocator)
+//   warp  9    tcgen05.mma issuer
+// TMEM (512 cols for D=128): S^T [0,128) (P^T bf16 in [0,64), then dQ_i),
+// dP^T [128,256), dV [256,256+D), dK [256+D,256+2D).
+#pragma once
+#include <cuda.h>
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace burst {
+namespace bwd {
+
+constexpr int BM = 128;  // query rows per iteration
+constexpr int BN = 128;  // key rows per CTA
+constexpr int kThreads = 384;   // 3 warpgroups (warps 10-11 idle) for setmaxnreg
+
+template <int D>
+struct Cfg {
+  static constexpr int kBoxBytes = 128 * 64 * 2;
+  static constexpr int kBoxes = D / 64;
+  static constexpr int kTileBytes = kBoxBytes * kBoxes;    // K, V, Q_i, dO_i tiles
+  static constexpr int kDsBytes = BN * BM * 2;              // dS^T tile (bf16)
+  static constexpr int kStatBytes = 2 * BM * 4;             // lse2_i, D_i
+  static constexpr int kPayload = 2 * kTileBytes + 2 * 2 * kTileBytes + kDsBytes + 2 * kStatBytes;
+  static constexpr int kBarBytes = 128;
+  static constexpr int kMaxSmem = 232448;
+  static constexpr int kSmemBytes =
+      (kPayload + kBarBytes + 1024 <= kMaxSmem) ? kPayload + kBarBytes + 1024 : kMaxSmem;
+  static constexpr int kMaxPad = kSmemBytes - kPayload - kBarBytes;
+};
+
+struct Params {
+  CUtensorMap tm_q, tm_k, tm_v, tm_do;
+  const float* stats;    // [2][B*H][NTq*128]: lse*log2e, D
+  float* dq_acc;         // TL over n_q
+  float* dk_acc;         // TL over n_k
+  float* dv_acc;
+  burst_hop hop;
+  float scale_log2, scale;
+  int accumulate;
+};
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          ptx::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(ptx::smem_u32(bar))
+      : "memory");
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_constant__ Params p) {
+  using C = Cfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem;
+  {
+    const uint32_t s = ptx::smem_u32(smem_raw);
+    const uint32_t pad = (1024u - (s & 1023u)) & 1023u;
+    if (pad > (uint32_t)C::kMaxPad) __trap();
+    smem = smem_raw + pad;
+  }
+  uint8_t* sK = smem;
+  uint8_t* sV = sK + C::kTileBytes;
+  uint8_t* sQ = sV + C::kTileBytes;            // [2] stages
+  uint8_t* sdO = sQ + 2 * C::kTileBytes;       // [2] stages
+  uint8_t* sdS = sdO + 2 * C::kTileBytes;
+  float* sStat = reinterpret_cast<float*>(sdS + C::kDsBytes);   // [2][2][BM]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sStat) + 2 * C::kStatBytes);
+  uint64_t* kv_full = bars;
+  uint64_t* qdo_full = bars + 1;   // [2]
+  uint64_t* qdo_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;
+  uint64_t* p_full = bars + 6;
+  uint64_t* ds_full = bars + 7;
+  uint64_t* ds_empty = bars + 8;
+  uint64_t* dq_full = bars + 9;
+  uint64_t* dq_empty = bars + 10;
+  uint64_t* dkv_full = bars + 11;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 12);
+
+  const burst_hop& hp = p.hop;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.z, h = blockIdx.y;
+  const int64_t bh = (int64_t)b * hp.heads + h;
+  const int64_t k0 = hp.k_begin + (int64_t)blockIdx.x * BN;   // first key row of this CTA
+  const int64_t k_end = hp.k_begin + hp.k_len;
+  const int64_t q_end = hp.q_begin + hp.q_len;
+  const int64_t NTq = ceil_div(hp.n_q, 128);
+  const int64_t NTk = ceil_div(hp.n_k, 128);
+
+  // Query tiles touching this key tile: causal => suffix of the hop's queries.
+  int64_t qs = hp.q_begin;
+  if (hp.causal) {
+    const int64_t first_q = count_le(hp.q_map, hp.n_q, pos_of(hp.k_map, k0) - 1);
+    if (first_q > qs) qs = hp.q_begin + ((first_q - hp.q_begin) / BM) * BM;
+  }
+  const int nq = qs < q_end ? (int)ceil_div(q_end - qs, BM) : 0;
+
+  if (warp == 8) {
+    if (lane == 0) {
+      ptx::mbar_init(kv_full, 1);
+      for (int s = 0; s < 2; ++s) {
+        ptx::mbar_init(qdo_full + s, 1);
+        ptx::mbar_init(qdo_empty + s, 1);
+      }
+      ptx::mbar_init(s_full, 1);
+      ptx::mbar_init(p_full, BN);
+      ptx::mbar_init(ds_full, BN);
+      ptx::mbar_init(ds_empty, 1);
+      ptx::mbar_init(dq_full, 1);
+      ptx::mbar_init(dq_empty, BM);
+      ptx::mbar_init(dkv_full, 1);
+      ptx::fence_mbar_init();
+      ptx::tma_prefetch_desc(&p.tm_q);
+      ptx::tma_prefetch_desc(&p.tm_k);
+      ptx::tma_prefetch_desc(&p.tm_v);
+      ptx::tma_prefetch_desc(&p.tm_do);
+    }
+    __syncwarp();
+    ptx::tmem_alloc(tmem_holder, 512);
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tbase = *tmem_holder;
+  constexpr uint32_t kS = 0, kDP = 128, kDV = 256, kDK = 256 + D;
+  if (warp >= 8) {
+   ptx::regs_dec<56>();
+   if (warp == 8) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0 && nq > 0) {
+      ptx::mbar_expect_tx(kv_full, 2 * C::kTileBytes);
+      for (int x = 0; x < C::kBoxes; ++x) {
+        ptx::tma_load_4d(sK + x * C::kBoxBytes, &p.tm_k, kv_full, x * 64, h, (int)k0, b);
+        ptx::tma_load_4d(sV + x * C::kBoxBytes, &p.tm_v, kv_full, x * 64, h, (int)k0, b);
+      }
+      for (int i = 0; i < nq; ++i) {
+        const int s = i & 1;
+        const int64_t q0 = qs + (int64_t)i * BM;
+        ptx::mbar_wait(qdo_empty + s, ((i >> 1) & 1) ^ 1);
+        ptx::mbar_expect_tx(qdo_full + s, 2 * C::kTileBytes + C::kStatBytes);
+        for (int x = 0; x < C::kBoxes; ++x) {
+          ptx::tma_load_4d(sQ + s * C::kTileBytes + x * C::kBoxBytes, &p.tm_q, qdo_full + s,
+                           x * 64, h, (int)q0, b);
+          ptx::tma_load_4d(sdO + s * C::kTileBytes + x * C::kBoxBytes, &p.tm_do, qdo_full + s,
+                           x * 64, h, (int)q0, b);
+        }
+        const float* st = p.stats + bh * NTq * 128 + q0;
+        bulk_load(sStat + s * 2 * BM, st, BM * 4, qdo_full + s);
+        bulk_load(sStat + s * 2 * BM + BM, st + (int64_t)hp.batch * hp.heads * NTq * 128, BM * 4,
+                  qdo_full + s);
+      }
+    }
+  } else if (warp == 9) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0 && nq > 0) {
+      constexpr uint32_t id_kk = ptx::make_idesc_bf16(BN, BM, 0, 0);   // S^T, dP^T
+      constexpr uint32_t id_kmn = ptx::make_idesc_bf16(BN, D, 0, 1);   // dV, dK (B MN-major)
+      constexpr uint32_t id_mnmn = ptx::make_idesc_bf16(BM, D, 1, 1);  // dQ (A, B MN-major)
+      const uint32_t aK = ptx::smem_u32(sK), aV = ptx::smem_u32(sV);
+      const uint32_t aQ = ptx::smem_u32(sQ), adO = ptx::smem_u32(sdO), adS = ptx::smem_u32(sdS);
+      ptx::mbar_wait(kv_full, 0);
+      for (int i = 0; i < nq; ++i) {
+        const int s = i & 1;
+        const uint32_t q = aQ + s * C::kTileBytes, dO = adO + s * C::kTileBytes;
+        ptx::mbar_wait(qdo_full + s, (i >> 1) & 1);
+        ptx::tc_fence_after();
+        // dP^T = V dO^T   (K-major both, reduction over D)
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * C::kBoxBytes + (kk & 3) * 32;
+          ptx::mma_ss(tbase + kDP, ptx::make_sdesc(aV + off, 0, 1024),
+                      ptx::make_sdesc(dO + off, 0, 1024), id_kk, kk > 0);
+        }
+        if (i > 0) {
+          ptx::mbar_wait(dq_empty, (i - 1) & 1);
+          ptx::tc_fence_after();
+        }
+        // S^T = K Q^T
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * C::kBoxBytes + (kk & 3) * 32;
+          ptx::mma_ss(tbase + kS, ptx::make_sdesc(aK + off, 0, 1024),
+                      ptx::make_sdesc(q + off, 0, 1024), id_kk, kk > 0);
+        }
+        ptx::mma_commit(s_full);
+        // dV += P^T dO   (A = P^T from TMEM, B = dO MN-major, reduction over queries)
+        ptx::mbar_wait(p_full, i & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < BM / 16; ++kk)
+          ptx::mma_ts(tbase + kDV, tbase + kS + kk * 8,
+                      ptx::make_sdesc(dO + kk * 2048, C::kBoxBytes, 1024), id_kmn,
+                      (i > 0 || kk > 0) ? 1u : 0u);
+        // dK += dS^T Q ; dQ_i = dS K
+        ptx::mbar_wait(ds_full, i & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < BM / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          ptx::mma_ss(tbase + kDK, ptx::make_sdesc(adS + off, 0, 1024),
+                      ptx::make_sdesc(q + kk * 2048, C::kBoxBytes, 1024), id_kmn,
+                      (i > 0 || kk > 0) ? 1u : 0u);
+        }
+#pragma unroll
+        for (int kk = 0; kk < BN / 16; ++kk)
+          ptx::mma_ss(tbase + kS, ptx::make_sdesc(adS + kk * 2048, 16384, 1024),
+                      ptx::make_sdesc(aK + kk * 2048, C::kBoxBytes, 1024), id_mnmn, kk > 0);
+        ptx::mma_commit(dq_full);
+        ptx::mma_commit(ds_empty);
+        ptx::mma_commit(qdo_empty + s);
+      }
+      ptx::mma_commit(dkv_full);
+    }
+   }
+  } else if (warp < 4) {
+    // ------------------------------------------------------------ P / dS warpgroup
+    ptx::regs_inc<240>();
+    const int t = threadIdx.x;                  // key row within the tile
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const int64_t krow = k0 + t;
+    const bool kvalid = krow < k_end && krow < hp.n_k;
+    const int64_t kpos = hp.causal ? pos_of(hp.k_map, kvalid ? krow : k0) : 0;
+    const int64_t qfirst = hp.causal ? count_le(hp.q_map, hp.n_q, kpos - 1) : 0;
+    const float c2 = p.scale_log2;
+    for (int i = 0; i < nq; ++i) {
+      const int s = i & 1;
+      const int64_t q0 = qs + (int64_t)i * BM;
+      // visible query columns of this key row: [lo, hi)
+      int64_t lo = qfirst - q0, hi = q_end - q0;
+      if (lo < 0) lo = 0;
+      if (hi > BM) hi = BM;
+      if (!kvalid) hi = 0;
+      ptx::mbar_wait(qdo_full + s, (i >> 1) & 1);
+      ptx::mbar_wait(s_full, i & 1);
+      ptx::tc_fence_after();
+      const float* lse2 = sStat + s * 2 * BM;
+      const float* dst = lse2 + BM;
+      float pr[BM];
+#pragma unroll
+      for (int cc = 0; cc < BM / 32; ++cc) {
+        uint32_t r[32];
+        ptx::tmem_ld32(tbase + lane_off + kS + cc * 32, r);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int c = cc * 32 + j;
+          const float e = ptx::ex2(fmaf(__uint_as_float(r[j]), c2, -lse2[c]));
+          pr[c] = (c >= lo && c < hi) ? e : 0.f;
+        }
+      }
+#pragma unroll
+      for (int cc = 0; cc < BM / 64; ++cc) {
+        uint32_t pk[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) pk[j] = ptx::pack_bf16(pr[cc * 64 + 2 * j], pr[cc * 64 + 2 * j + 1]);
+        ptx::tmem_st32(tbase + lane_off + kS + cc * 32, pk);
+      }
+      ptx::tmem_wait_st();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(p_full);
+
+      ptx::mbar_wait(ds_empty, (i & 1) ^ 1);
+#pragma unroll
+      for (int cc = 0; cc < BM / 32; ++cc) {
+        uint32_t r[32];
+        ptx::tmem_ld32(tbase + lane_off + kDP + cc * 32, r);
+        ptx::tmem_wait_ld();
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int c = cc * 32 + 2 * j;
+          const float d0 = pr[c] * (__uint_as_float(r[2 * j]) - dst[c]);
+          const float d1 = pr[c + 1] * (__uint_as_float(r[2 * j + 1]) - dst[c + 1]);
+          pk[j] = ptx::pack_bf16(d0, d1);
+        }
+        // SW128 K-major: row t, query chunk (16 B = 8 bf16) index ch in [0,8) of half x
+        uint8_t* rowp = sdS + (cc >> 1) * 16384 + t * 128;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int ch = (cc & 1) * 4 + u;
+          *reinterpret_cast<uint4*>(rowp + ((ch ^ (t & 7)) << 4)) =
+              make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        }
+      }
+      ptx::fence_proxy_async_smem();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(ds_full);
+    }
+    // -------------------------------------------------------- dK / dV epilogue
+    if (nq > 0) {
+      ptx::mbar_wait(dkv_full, 0);
+      ptx::tc_fence_after();
+    }
+#pragma unroll 1
+    for (int which = 0; which < 2; ++which) {
+      float* dst = which == 0 ? p.dv_acc : p.dk_acc;
+      const float mul = which == 0 ? 1.f : p.scale;
+      const uint32_t col0 = which == 0 ? kDV : kDK;
+#pragma unroll
+      for (int cc = 0; cc < D / 32; ++cc) {
+        uint32_t r[32];
+        if (nq > 0) {
+          ptx::tmem_ld32(tbase + lane_off + col0 + cc * 32, r);
+          ptx::tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r[j] = 0u;
+        }
+        if (!kvalid) continue;
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          float4* a = reinterpret_cast<float4*>(dst + tl_index(bh, krow, cc * 32 + j, D, NTk));
+          float4 v = make_float4(__uint_as_float(r[j]) * mul, __uint_as_float(r[j + 1]) * mul,
+                                 __uint_as_float(r[j + 2]) * mul, __uint_as_float(r[j + 3]) * mul);
+          if (p.accumulate) {
+            const float4 o = *a;
+            v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+          }
+          *a = v;
+        }
+      }
+    }
+  } else if (warp < 8) {
+    // ------------------------------------------------------------ dQ drain warpgroup
+    const int t = threadIdx.x & 127;           // query row within the tile
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    for (int i = 0; i < nq; ++i) {
+      const int64_t qrow = qs + (int64_t)i * BM + t;
+      const bool qvalid = qrow < q_end && qrow < hp.n_q;
+      ptx::mbar_wait(dq_full, i & 1);
+      ptx::tc_fence_after();
+#pragma unroll
+      for (int cc = 0; cc < D / 32; ++cc) {
+        uint32_t r[32];
+        ptx::tmem_ld32(tbase + lane_off + kS + cc * 32, r);
+        ptx::tmem_wait_ld();
+        if (cc == D / 32 - 1) {
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(dq_empty);
+        }
+        if (qvalid) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            ptx::red_add_v4(p.dq_acc + tl_index(bh, qrow, cc * 32 + j, D, NTq),
+                            __uint_as_float(r[j]) * p.scale, __uint_as_float(r[j + 1]) * p.scale,
+                            __uint_as_float(r[j + 2]) * p.scale, __uint_as_float(r[j + 3]) * p.scale);
+        }
+      }
+    }
+  }
+
+  __syncwarp();
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 8) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tbase, 512);
+  }
+}
+
+}  // namespace bwd
+}  // namespace burst

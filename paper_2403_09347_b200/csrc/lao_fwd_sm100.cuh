@@ -1,0 +1,362 @@
+// LAO forward on sm_100a: TMA -> SMEM (128B swizzle) -> tcgen05.mma -> TMEM,
+// online softmax in registers, P written back to TMEM and consumed by a
+// TMEM-operand MMA, GAO merge with the running (O_acc, m, l) state fused into
+// the epilogue.
+//
+// Reference semantics: one call = ring.forward_step (ring.py:158-181) for every
+// (batch, head) slice: local_forward_tiled (local_attn.py:207-248) over the
+// hop's rectangle followed by PartialAttn.merge into the device state
+// (local_attn.py:101-120), and on the last hop PartialAttn.finalize
+// (local_attn.py:127-135).  Scores use S * scale * log2(e) with exp2; the state
+// keeps m in log2 units; lse is converted back to natural log.
+//
+// CTA = 2 query tiles of 128 rows sharing every K/V tile (halves K/V SMEM and
+// L2 traffic per FLOP and lets one tile's softmax overlap the other's MMAs).
+//   warps 0-3  softmax/epilogue for query tile 0 (thread = row = TMEM lane)
+//   warps 4-7  softmax/epilogue for query tile 1
+//   warp  8    TMA producer (+ TMEM allocator)
+//   warp  9    tcgen05.mma issuer (one elected lane)
+// TMEM (512 cols): S0 [0,128) S1 [128,256) O0 [256,256+D) O1 [256+D,256+2D);
+// P_t (bf16, 64 cols) aliases the first half of S_t.
+#pragma once
+#include <cuda.h>
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace burst {
+namespace fwd {
+
+constexpr int BM = 128;       // query rows per tile
+constexpr int BN = 128;       // keys per tile
+constexpr int kThreads = 384;   // 3 warpgroups (warps 10-11 idle) for setmaxnreg
+constexpr float kRescaleThreshold = 8.0f;  // log2 units: lazy rescale (values <= 2^8)
+
+template <int D>
+struct Cfg {
+  static constexpr int kBoxBytes = 128 * 64 * 2;      // one TMA box: 128 rows x 64 bf16
+  static constexpr int kBoxes = D / 64;
+  static constexpr int kTileBytes = kBoxBytes * kBoxes;
+  static constexpr int kStages = (D == 128) ? 4 : 6;
+  static constexpr int kSmemBytes = 1024 + 2 * kTileBytes + kStages * kTileBytes + 256;
+};
+
+struct Params {
+  CUtensorMap tm_q, tm_k, tm_v;
+  float* o_acc;
+  float* m_run;
+  float* l_run;
+  void* o_out;
+  float* lse_out;
+  int* flags;
+  burst_hop hop;
+  float scale_log2;
+  int first_hop, finalize;
+};
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+  uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  uint32_t s = ptx::smem_u32(p);
+  uint32_t pad = (1024u - (s & 1023u)) & 1023u;
+  return reinterpret_cast<uint8_t*>(a + pad);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_constant__ Params p) {
+  using C = Cfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* sQ = smem;                          // 2 tiles
+  uint8_t* sKV = smem + 2 * C::kTileBytes;     // kStages slots (K_j, V_j alternate)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::kStages * C::kTileBytes);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_empty = kv_full + C::kStages;
+  uint64_t* s_full = kv_empty + C::kStages;   // [2]
+  uint64_t* p_full = s_full + 2;              // [2]
+  uint64_t* o_full = p_full + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_full + 1);
+
+  const burst_hop& hp = p.hop;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.z, h = blockIdx.y;
+  const int64_t q_end = hp.q_begin + hp.q_len;
+  const int64_t row0 = hp.q_begin + (int64_t)blockIdx.x * (2 * BM);
+
+  // Key span this CTA needs: causal => a prefix of the hop's keys (monotone maps).
+  int64_t kspan = hp.k_len;
+  if (hp.causal) {
+    int64_t last = (row0 + 2 * BM < q_end ? row0 + 2 * BM : q_end) - 1;
+    int64_t cnt = count_le(hp.k_map, hp.n_k, pos_of(hp.q_map, last)) - hp.k_begin;
+    kspan = cnt < kspan ? cnt : kspan;
+    if (kspan < 0) kspan = 0;
+  }
+  const int nkv = (int)ceil_div(kspan, BN);
+
+  if (warp == 8) {
+    if (lane == 0) {
+      ptx::mbar_init(q_full, 1);
+      for (int s = 0; s < C::kStages; ++s) {
+        ptx::mbar_init(kv_full + s, 1);
+        ptx::mbar_init(kv_empty + s, 1);
+      }
+      for (int t = 0; t < 2; ++t) {
+        ptx::mbar_init(s_full + t, 1);
+        ptx::mbar_init(p_full + t, BM);
+      }
+      ptx::mbar_init(o_full, 1);
+      ptx::fence_mbar_init();
+      ptx::tma_prefetch_desc(&p.tm_q);
+      ptx::tma_prefetch_desc(&p.tm_k);
+      ptx::tma_prefetch_desc(&p.tm_v);
+    }
+    __syncwarp();
+    ptx::tmem_alloc(tmem_holder, 512);
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tbase = *tmem_holder;
+  if (warp >= 8) {
+   ptx::regs_dec<56>();
+   if (warp == 8) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0 && nkv > 0) {
+      ptx::mbar_expect_tx(q_full, 2 * C::kTileBytes);
+      for (int t = 0; t < 2; ++t)
+        for (int x = 0; x < C::kBoxes; ++x)
+          ptx::tma_load_4d(sQ + t * C::kTileBytes + x * C::kBoxBytes, &p.tm_q, q_full, x * 64, h,
+                           (int)(row0 + t * BM), b);
+      int it = 0;
+      for (int j = 0; j < nkv; ++j) {
+        const int krow = (int)(hp.k_begin + (int64_t)j * BN);
+        for (int kv = 0; kv < 2; ++kv, ++it) {
+          const int s = it % C::kStages;
+          const uint32_t use = it / C::kStages;
+          ptx::mbar_wait(kv_empty + s, (use & 1) ^ 1);
+          ptx::mbar_expect_tx(kv_full + s, C::kTileBytes);
+          const CUtensorMap* tm = kv == 0 ? &p.tm_k : &p.tm_v;
+          for (int x = 0; x < C::kBoxes; ++x)
+            ptx::tma_load_4d(sKV + s * C::kTileBytes + x * C::kBoxBytes, tm, kv_full + s, x * 64,
+                             h, krow, b);
+        }
+      }
+    }
+  } else if (warp == 9) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0 && nkv > 0) {
+      constexpr uint32_t idesc_qk = ptx::make_idesc_bf16(BM, BN, 0, 0);
+      constexpr uint32_t idesc_pv = ptx::make_idesc_bf16(BM, D, 0, 1);
+      const uint32_t sQa = ptx::smem_u32(sQ);
+      const uint32_t sKVa = ptx::smem_u32(sKV);
+      auto qk = [&](int t, int slot) {
+        const uint32_t qa = sQa + t * C::kTileBytes;
+        const uint32_t ka = sKVa + slot * C::kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * C::kBoxBytes + (kk & 3) * 32;
+          ptx::mma_ss(tbase + t * 128, ptx::make_sdesc(qa + off, 0, 1024),
+                      ptx::make_sdesc(ka + off, 0, 1024), idesc_qk, kk > 0);
+        }
+      };
+      auto pv = [&](int t, int slot, bool acc) {
+        const uint32_t va = sKVa + slot * C::kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < BN / 16; ++kk) {
+          ptx::mma_ts(tbase + 256 + t * D, tbase + t * 128 + kk * 8,
+                      ptx::make_sdesc(va + kk * 2048, C::kBoxBytes, 1024), idesc_pv,
+                      (acc || kk > 0) ? 1u : 0u);
+        }
+      };
+      ptx::mbar_wait(q_full, 0);
+      ptx::mbar_wait(kv_full + 0, 0);
+      ptx::tc_fence_after();
+      qk(0, 0);
+      ptx::mma_commit(s_full + 0);
+      qk(1, 0);
+      ptx::mma_commit(s_full + 1);
+      ptx::mma_commit(kv_empty + 0);
+      for (int j = 0; j < nkv; ++j) {
+        const int itv = 2 * j + 1, sv = itv % C::kStages;
+        const int itk = 2 * j + 2, sk = itk % C::kStages;
+        const bool more = j + 1 < nkv;
+        ptx::mbar_wait(kv_full + sv, (itv / C::kStages) & 1);
+        ptx::mbar_wait(p_full + 0, j & 1);
+        ptx::tc_fence_after();
+        pv(0, sv, j > 0);
+        if (more) {
+          ptx::mbar_wait(kv_full + sk, (itk / C::kStages) & 1);
+          ptx::tc_fence_after();
+          qk(0, sk);
+          ptx::mma_commit(s_full + 0);
+        }
+        ptx::mbar_wait(p_full + 1, j & 1);
+        ptx::tc_fence_after();
+        pv(1, sv, j > 0);
+        ptx::mma_commit(kv_empty + sv);
+        if (more) {
+          qk(1, sk);
+          ptx::mma_commit(s_full + 1);
+          ptx::mma_commit(kv_empty + sk);
+        }
+      }
+      ptx::mma_commit(o_full);
+    }
+   }
+  } else {
+    // ------------------------------------------------------------ softmax WGs
+    ptx::regs_inc<224>();
+    const int g = warp >> 2;                 // query tile 0/1
+    const int t = threadIdx.x & 127;         // row within the tile = TMEM lane
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t tS = tbase + lane_off + g * 128;
+    const uint32_t tO = tbase + lane_off + 256 + g * D;
+    const int64_t row = row0 + g * BM + t;
+    const bool valid = row < q_end && row < hp.n_q;
+    // keys visible to this row, relative to the hop's k_begin
+    int64_t lim = hp.k_len;
+    if (hp.causal) {
+      int64_t cnt = count_le(hp.k_map, hp.n_k, pos_of(hp.q_map, valid ? row : q_end - 1)) -
+                    hp.k_begin;
+      lim = cnt < lim ? cnt : lim;
+    }
+    const float c2 = p.scale_log2;
+    float m_run = -INFINITY, l_run = 0.f;
+
+    for (int j = 0; j < nkv; ++j) {
+      ptx::mbar_wait(s_full + g, j & 1);
+      ptx::tc_fence_after();
+      float s[BN];
+#pragma unroll
+      for (int cc = 0; cc < BN / 32; ++cc) {
+        uint32_t r[32];
+        ptx::tmem_ld32(tS + cc * 32, r);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[cc * 32 + i] = __uint_as_float(r[i]);
+      }
+      ptx::tmem_wait_ld();
+      const int64_t nvalid = lim - (int64_t)j * BN;
+      if (__any_sync(0xffffffffu, nvalid < BN)) {
+#pragma unroll
+        for (int i = 0; i < BN; ++i)
+          if (i >= nvalid) s[i] = -INFINITY;
+      }
+      float mx = s[0];
+#pragma unroll
+      for (int i = 1; i < BN; ++i) mx = fmaxf(mx, s[i]);
+      const float m_tile = mx * c2;
+      const bool grow = m_tile > m_run + kRescaleThreshold || (m_run == -INFINITY && m_tile > -INFINITY);
+      if (__any_sync(0xffffffffu, grow && j > 0)) {
+        const float m_new = grow ? fmaxf(m_tile, m_run) : m_run;
+        const float alpha = (m_run == -INFINITY) ? 0.f : ptx::ex2(m_run - m_new);
+#pragma unroll
+        for (int cc = 0; cc < D / 32; ++cc) {
+          uint32_t r[32];
+          ptx::tmem_ld32(tO + cc * 32, r);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+          ptx::tmem_st32(tO + cc * 32, r);
+        }
+        l_run *= alpha;
+        m_run = m_new;
+      } else if (grow) {
+        m_run = fmaxf(m_tile, m_run);
+      }
+      const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+      float lsum = 0.f;
+#pragma unroll
+      for (int cc = 0; cc < BN / 64; ++cc) {
+        uint32_t pk[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float p0 = ptx::ex2(fmaf(s[cc * 64 + 2 * i], c2, -m_use));
+          const float p1 = ptx::ex2(fmaf(s[cc * 64 + 2 * i + 1], c2, -m_use));
+          lsum += p0 + p1;
+          pk[i] = ptx::pack_bf16(p0, p1);
+        }
+        ptx::tmem_st32(tS + cc * 32, pk);
+      }
+      l_run += lsum;
+      ptx::tmem_wait_st();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(p_full + g);
+    }
+
+    // ------------------------------------------------------------ epilogue
+    if (nkv > 0) {
+      ptx::mbar_wait(o_full, 0);
+      ptx::tc_fence_after();
+    }
+    const int64_t bh = (int64_t)b * hp.heads + h;
+    const int64_t NT = ceil_div(hp.n_q, 128);
+    float m_old = -INFINITY, l_old = 0.f;
+    if (valid && !p.first_hop) {
+      m_old = p.m_run[bh * hp.n_q + row];
+      l_old = p.l_run[bh * hp.n_q + row];
+    }
+    const float m_new = fmaxf(m_old, m_run);
+    const float a_old = (m_old == -INFINITY) ? 0.f : ptx::ex2(m_old - m_new);
+    const float a_hop = (m_run == -INFINITY) ? 0.f : ptx::ex2(m_run - m_new);
+    const float l_new = a_old * l_old + a_hop * l_run;
+    const float inv_l = (l_new > 0.f) ? 1.f / l_new : 0.f;
+    if (valid && p.finalize && !(l_new > 0.f)) atomicOr(p.flags, 1);
+#pragma unroll
+    for (int cc = 0; cc < D / 32; ++cc) {
+      uint32_t r[32];
+      if (nkv > 0) {
+        ptx::tmem_ld32(tO + cc * 32, r);
+        ptx::tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) r[i] = 0u;
+      }
+      if (!valid) continue;
+      float o[32];
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        float4 prev = make_float4(0.f, 0.f, 0.f, 0.f);
+        const size_t ti = tl_index(bh, row, cc * 32 + i, D, NT);
+        if (!p.first_hop) prev = *reinterpret_cast<const float4*>(p.o_acc + ti);
+        o[i + 0] = a_old * prev.x + a_hop * __uint_as_float(r[i + 0]);
+        o[i + 1] = a_old * prev.y + a_hop * __uint_as_float(r[i + 1]);
+        o[i + 2] = a_old * prev.z + a_hop * __uint_as_float(r[i + 2]);
+        o[i + 3] = a_old * prev.w + a_hop * __uint_as_float(r[i + 3]);
+        if (!p.finalize)
+          *reinterpret_cast<float4*>(p.o_acc + ti) = make_float4(o[i], o[i + 1], o[i + 2], o[i + 3]);
+      }
+      if (p.finalize) {
+        __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.o_out) +
+                             (((int64_t)b * hp.n_q + row) * hp.heads + h) * D + cc * 32;
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 w;
+          w.x = ptx::pack_bf16(o[i + 0] * inv_l, o[i + 1] * inv_l);
+          w.y = ptx::pack_bf16(o[i + 2] * inv_l, o[i + 3] * inv_l);
+          w.z = ptx::pack_bf16(o[i + 4] * inv_l, o[i + 5] * inv_l);
+          w.w = ptx::pack_bf16(o[i + 6] * inv_l, o[i + 7] * inv_l);
+          *reinterpret_cast<uint4*>(out + i) = w;
+        }
+      }
+    }
+    if (valid) {
+      if (p.finalize) {
+        p.lse_out[bh * hp.n_q + row] = (l_new > 0.f) ? (m_new + __log2f(l_new)) * kLn2 : -INFINITY;
+      } else {
+        p.m_run[bh * hp.n_q + row] = m_new;
+        p.l_run[bh * hp.n_q + row] = l_new;
+      }
+    }
+  }
+
+  __syncwarp();
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 8) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tbase, 512);
+  }
+}
+
+}  // namespace fwd
+}  // namespace burst

@@ -1,0 +1,169 @@
+"""Kernel provider: torch tensors in, C-ABI (libburst_b200.so) calls out.
+
+This is the ONLY compute provider of the product.  Every method checks that
+its tensors live on a CUDA device and raises otherwise: there is no CPU path.
+The ring engine (`ring.py`) sees the running forward state and backward
+workspaces as opaque objects created here.
+
+Mapping onto the reference (pkg/src/burstsim):
+  fwd           ring.forward_step -> local_forward_tiled + PartialAttn.merge
+  fwd_finalize  PartialAttn.finalize / ring.finalize_forward
+  bwd_prepare   ring.init_backward (D = rowsum(dO * O), zeroed dQ accumulator)
+  bwd           ring.backward_step -> local_backward
+  bwd_finalize  sim._collect (dQ home, dK/dV summed)
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from .errors import CudaError, ShapeError
+from .schedule import HopPlan
+
+_DTYPES = {torch.bfloat16: _lib.DTYPE_BF16, torch.float32: _lib.DTYPE_F32}
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _stream_handle(stream) -> ctypes.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def dtype_code(t: torch.Tensor) -> int:
+    try:
+        return _DTYPES[t.dtype]
+    except KeyError:
+        raise ShapeError(f"unsupported dtype {t.dtype}; use bfloat16 or float32") from None
+
+
+def check_qkv(q, k, v) -> tuple[int, int, int, int]:
+    """[B, n, H, D] contiguous CUDA tensors of one dtype (dense.py:34-46 checks)."""
+    for name, t in (("q", q), ("k", k), ("v", v)):
+        if not t.is_cuda:
+            raise CudaError(f"{name} is on {t.device}: the BurstAttention path runs only on CUDA "
+                            "(sm_100a); there is no CPU fallback")
+        if t.dim() != 4:
+            raise ShapeError(f"{name} must be [batch, seq, heads, head_dim], got {tuple(t.shape)}")
+        if not t.is_contiguous():
+            raise ShapeError(f"{name} must be contiguous")
+    if q.dtype != k.dtype or q.dtype != v.dtype:
+        raise ShapeError("mixed dtypes across Q, K, V")
+    if k.shape != v.shape or q.shape[0] != k.shape[0] or q.shape[2:] != k.shape[2:]:
+        raise ShapeError(f"incompatible shapes Q={tuple(q.shape)} K={tuple(k.shape)} "
+                         f"V={tuple(v.shape)}")
+    B, n, H, D = q.shape
+    if n < 1 or k.shape[1] < 1:
+        raise ShapeError("empty attention block")
+    dtype_code(q)
+    return B, n, H, D
+
+
+def ws_floats(B: int, H: int, D: int, n: int) -> int:
+    return B * H * (-(-n // 128) * 128) * D
+
+
+@dataclass
+class FwdState:
+    """Running (O_acc, m, l) of the pinned query block (PartialAttn, local_attn.py:66-99)."""
+    o_acc: torch.Tensor   # TL fp32 workspace
+    m: torch.Tensor       # [B, H, n] fp32, log2 units
+    l: torch.Tensor       # [B, H, n] fp32
+
+
+@dataclass
+class BwdState:
+    stats: torch.Tensor   # [2, B*H, ceil(n/128)*128]: lse*log2e, D
+    dq_acc: torch.Tensor  # TL fp32
+
+
+def make_hop(plan: HopPlan, q: torch.Tensor, k: torch.Tensor, scale: float) -> _lib.Hop:
+    B, n_q, H, D = q.shape
+    h = _lib.Hop()
+    h.batch, h.heads, h.head_dim, h.dtype = B, H, D, dtype_code(q)
+    h.n_q, h.n_k = n_q, k.shape[1]
+    h.q_begin, h.q_len, h.k_begin, h.k_len = plan.q_begin, plan.q_len, plan.k_begin, plan.k_len
+    h.softmax_scale = float(scale)
+    h.causal = 1 if plan.causal else 0
+    h.q_map = _lib.PosMap(plan.q_map.pos0, plan.q_map.pos1, plan.q_map.seg_len)
+    h.k_map = _lib.PosMap(plan.k_map.pos0, plan.k_map.pos1, plan.k_map.seg_len)
+    return h
+
+
+class CudaKernels:
+    """sm_100a kernels behind the C ABI (tcgen05 bf16 / SIMT f32)."""
+
+    name = "cuda"
+
+    def __init__(self):
+        _lib.load()
+
+    # ------------------------------------------------------------ allocation
+    def fwd_state(self, q: torch.Tensor) -> FwdState:
+        B, n, H, D = q.shape
+        dev = q.device
+        return FwdState(torch.empty(ws_floats(B, H, D, n), dtype=torch.float32, device=dev),
+                        torch.empty(B, H, n, dtype=torch.float32, device=dev),
+                        torch.empty(B, H, n, dtype=torch.float32, device=dev))
+
+    def part(self, k: torch.Tensor) -> torch.Tensor:
+        """One fp32 dK or dV contribution buffer for a visiting block (TL layout)."""
+        B, n, H, D = k.shape
+        return torch.empty(ws_floats(B, H, D, n), dtype=torch.float32, device=k.device)
+
+    # ------------------------------------------------------------ forward
+    def fwd(self, plan: HopPlan, q, k, v, scale: float, state: FwdState | None, o, lse,
+            first: bool, finalize: bool, stream=None) -> None:
+        hop = make_hop(plan, q, k, scale)
+        _lib.call("burst_lao_fwd", ctypes.byref(hop), _ptr(q), _ptr(k), _ptr(v),
+                  _ptr(state.o_acc if state else None), _ptr(state.m if state else None),
+                  _ptr(state.l if state else None), _ptr(o if finalize else None),
+                  _ptr(lse if finalize else None), int(first), int(finalize),
+                  _stream_handle(stream))
+
+    def fwd_finalize(self, state: FwdState, o, lse, stream=None) -> None:
+        B, n, H, D = o.shape
+        _lib.call("burst_fwd_finalize", dtype_code(o), B, H, D, n, _ptr(state.o_acc),
+                  _ptr(state.m), _ptr(state.l), _ptr(o), _ptr(lse), _stream_handle(stream))
+
+    # ------------------------------------------------------------ backward
+    def bwd_prepare(self, o, dout, lse, stream=None) -> BwdState:
+        B, n, H, D = o.shape
+        nt = -(-n // 128) * 128
+        st = BwdState(torch.empty(2, B * H, nt, dtype=torch.float32, device=o.device),
+                      torch.empty(ws_floats(B, H, D, n), dtype=torch.float32, device=o.device))
+        _lib.call("burst_bwd_preprocess", dtype_code(o), B, H, D, n, _ptr(o), _ptr(dout),
+                  _ptr(lse), _ptr(st.stats), _ptr(st.dq_acc), _stream_handle(stream))
+        return st
+
+    def bwd(self, plan: HopPlan, q, k, v, dout, scale: float, st: BwdState, dk_part, dv_part,
+            accumulate: bool, stream=None) -> None:
+        hop = make_hop(plan, q, k, scale)
+        _lib.call("burst_lao_bwd", ctypes.byref(hop), _ptr(q), _ptr(k), _ptr(v), _ptr(dout),
+                  _ptr(st.stats), _ptr(st.dq_acc), _ptr(dk_part), _ptr(dv_part), int(accumulate),
+                  _stream_handle(stream))
+
+    def bwd_finalize(self, st: BwdState, dk_parts, dv_parts, dq, dk, dv, stream=None) -> None:
+        B, n, H, D = dq.shape
+        np_ = len(dk_parts)
+        arr_k = (ctypes.c_void_p * max(np_, 1))(*[p.data_ptr() for p in dk_parts])
+        arr_v = (ctypes.c_void_p * max(np_, 1))(*[p.data_ptr() for p in dv_parts])
+        _lib.call("burst_bwd_finalize", dtype_code(dq), B, H, D, n, _ptr(st.dq_acc), arr_k, arr_v,
+                  np_, _ptr(dq), _ptr(dk), _ptr(dv), _stream_handle(stream))
+
+    def read_flags(self, stream=None) -> int:
+        out = ctypes.c_int32(0)
+        _lib.call("burst_read_flags", _stream_handle(stream), ctypes.byref(out))
+        return out.value
+
+
+def default_scale(head_dim: int) -> float:
+    """softmax scale d^-0.5 (runner.py:154)."""
+    return 1.0 / math.sqrt(head_dim)

@@ -1,0 +1,398 @@
+"""Ring engine: the per-rank hop loop of BurstAttention (GAO) with overlap.
+
+Reference: the lockstep / threaded executors of sim.run_ring_pass
+(sim.py:501-657): G rounds; at round r device i holds the payload of origin
+(i - r) mod G; payloads move i -> i+1 through double buffers
+(DoubleBuffer, sim.py:316-332).  Here one process (or thread) drives one rank:
+
+forward, hop h:   comm stream:    send K/V(h) -> rank+1, recv K/V(h+1) <- rank-1
+                  compute stream: LAO-fwd(q, K/V(h)) merged into (O_acc, m, l)
+backward, hop h:  comm stream:    K/V rotation as above, plus the dK/dV
+                                  contribution of hop h-1 sent to its home rank
+                                  (one hop behind, so it overlaps hop h)
+                  compute stream: LAO-bwd(q, dO, K/V(h)) -> dQ (pinned, fp32
+                                  atomics) and dK/dV(h) contribution
+                  end:            dK/dV = own + received contributions
+The compute stream only waits for a transfer right before the hop that
+consumes it, so every transfer except the last one overlaps a hop's kernel.
+
+Transports:
+  NcclTransport        one NCCL communicator via the C ABI (burst_ring_*); GPU
+  LoopbackTransport    G ranks as threads in one process (the reference's
+                       threaded executor); single-GPU simulation of a ring
+  TorchDistTransport   torch.distributed P2P (gloo on CPU for host-logic tests)
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from collections import defaultdict
+from typing import Sequence
+
+import torch
+
+from . import _lib
+from .errors import DeadlockError, RingDesyncError
+from .schedule import contributor_to, plan_hop
+
+SEND, RECV = "send", "recv"
+
+# ---------------------------------------------------------------------------
+# streams
+# ---------------------------------------------------------------------------
+
+_tls = threading.local()
+
+
+def comm_stream(device: torch.device):
+    """Per-thread, per-device high-priority communication stream."""
+    cache = getattr(_tls, "streams", None)
+    if cache is None:
+        cache = _tls.streams = {}
+    key = device.index if device.index is not None else torch.cuda.current_device()
+    if key not in cache:
+        cache[key] = torch.cuda.Stream(device=key, priority=-1)
+    return cache[key]
+
+
+class _Streams:
+    """Compute stream = caller's current stream; comm stream = side stream.
+    On CPU tensors (host-logic tests) everything is synchronous."""
+
+    def __init__(self, device: torch.device):
+        self.cuda = device.type == "cuda"
+        if self.cuda:
+            self.compute = torch.cuda.current_stream(device)
+            self.comm = comm_stream(device)
+        else:
+            self.compute = self.comm = None
+
+    def comm_after_compute(self):
+        if self.cuda:
+            self.comm.wait_stream(self.compute)
+
+    def compute_after_comm(self):
+        if self.cuda:
+            self.compute.wait_stream(self.comm)
+
+
+# ---------------------------------------------------------------------------
+# transports
+# ---------------------------------------------------------------------------
+
+class SoloTransport:
+    rank, world = 0, 1
+
+    def sendrecv(self, ops, stream):
+        if ops:
+            raise RingDesyncError("a world of one rank has nobody to exchange with")
+
+
+class NcclTransport:
+    """NCCL communicator owned by libburst_b200.so (burst_ring_create)."""
+
+    def __init__(self, group=None, device: torch.device | None = None):
+        import torch.distributed as dist
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        uid = (ctypes.c_char * 128)()
+        if self.rank == 0:
+            _lib.call("burst_ring_unique_id", uid)
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group else 0,
+                                   group=group)
+        uid = (ctypes.c_char * 128).from_buffer_copy(obj[0])
+        handle = ctypes.c_void_p()
+        _lib.call("burst_ring_create", uid, self.rank, self.world, dev.index, ctypes.byref(handle))
+        self.handle = handle
+
+    def sendrecv(self, ops, stream):
+        arr = (_lib.P2POp * len(ops))()
+        for i, (kind, t, peer) in enumerate(ops):
+            arr[i].buf = t.data_ptr()
+            arr[i].bytes = t.numel() * t.element_size()
+            arr[i].peer = peer
+            arr[i].is_send = 1 if kind == SEND else 0
+        _lib.call("burst_ring_sendrecv", self.handle, arr, len(ops),
+                  ctypes.c_void_p(stream.cuda_stream))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _lib.load().burst_ring_destroy(self.handle)
+            self.handle = None
+
+
+class TorchDistTransport:
+    """torch.distributed P2P (gloo on CPU: the multi-process host-logic tests)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def _global(self, peer):
+        return self.dist.get_global_rank(self.group, peer) if self.group is not None else peer
+
+    def sendrecv(self, ops, stream):
+        d = self.dist
+        p2p = [d.P2POp(d.isend if kind == SEND else d.irecv, t, self._global(peer), self.group)
+               for kind, t, peer in ops]
+        if not p2p:
+            return
+        ctx = torch.cuda.stream(stream) if stream is not None else _nullctx()
+        with ctx:
+            for req in d.batch_isend_irecv(p2p):
+                req.wait()
+
+
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+class LoopbackHub:
+    """Mailboxes + barrier shared by the G rank-threads of one process."""
+
+    def __init__(self, world: int, timeout: float = 120.0):
+        self.world = world
+        self.barrier = threading.Barrier(world, timeout=timeout)
+        self.lock = threading.Lock()
+        self.box = defaultdict(list)    # (seq, src, dst) -> [(tensor, event)]
+        self.copied = defaultdict(list)  # (seq, src) -> [events of finished copies]
+
+    def transport(self, rank: int) -> "LoopbackTransport":
+        return LoopbackTransport(self, rank)
+
+
+class LoopbackTransport:
+    """One rank of a LoopbackHub: device-to-device copies on the comm stream,
+    ordered with CUDA events exactly like a real send/recv (RingChannel,
+    sim.py:281-313; DeadlockError on a stalled peer, sim.py:290-310)."""
+
+    def __init__(self, hub: LoopbackHub, rank: int):
+        self.hub, self.rank, self.world = hub, rank, hub.world
+        self.seq = 0
+
+    def _sync(self):
+        try:
+            self.hub.barrier.wait()
+        except threading.BrokenBarrierError as e:
+            raise DeadlockError(f"rank {self.rank}: ring peer did not arrive") from e
+
+    def sendrecv(self, ops, stream):
+        hub, seq = self.hub, self.seq
+        self.seq += 1
+        cuda = stream is not None
+        with hub.lock:
+            for kind, t, peer in ops:
+                if kind == SEND:
+                    ev = None
+                    if cuda:
+                        ev = torch.cuda.Event()
+                        ev.record(stream)
+                    hub.box[(seq, self.rank, peer)].append((t, ev))
+        self._sync()
+        taken = defaultdict(int)
+        for kind, t, peer in ops:
+            if kind != RECV:
+                continue
+            with hub.lock:
+                items = hub.box.get((seq, peer, self.rank), [])
+                if taken[peer] >= len(items):
+                    raise RingDesyncError(f"rank {self.rank}: no payload from {peer} (seq {seq})")
+                src, ev = items[taken[peer]]
+            taken[peer] += 1
+            if src.shape != t.shape or src.dtype != t.dtype:
+                raise RingDesyncError(f"rank {self.rank}: payload from {peer} is "
+                                      f"{tuple(src.shape)}/{src.dtype}, expected "
+                                      f"{tuple(t.shape)}/{t.dtype}")
+            if cuda:
+                stream.wait_event(ev)
+                with torch.cuda.stream(stream):
+                    t.copy_(src, non_blocking=True)
+                done = torch.cuda.Event()
+                done.record(stream)
+            else:
+                t.copy_(src)
+                done = None
+            with hub.lock:
+                hub.copied[(seq, peer)].append(done)
+        self._sync()
+        if cuda:
+            # the sender may reuse its buffers only after every receiver copied
+            for ev in hub.copied.get((seq, self.rank), []):
+                stream.wait_event(ev)
+        self._sync()
+        with hub.lock:
+            for dst in range(self.world):
+                hub.box.pop((seq, self.rank, dst), None)
+            hub.copied.pop((seq, self.rank), None)
+
+
+# ---------------------------------------------------------------------------
+# the hop loops
+# ---------------------------------------------------------------------------
+
+def ring_forward(q, k, v, scale: float, causal: bool, zigzag: bool, transport, kernels):
+    """One rank's forward pass.  Returns (O [B,n,H,D], lse [B,H,n] natural log)."""
+    B, n, H, D = q.shape
+    G, r = transport.world, transport.rank
+    S = _Streams(q.device)
+    o = torch.empty_like(q)
+    lse = torch.empty(B, H, n, dtype=torch.float32, device=q.device)
+    state = kernels.fwd_state(q) if G > 1 else None
+    cur_k, cur_v = k, v
+    spare = None
+    finalized = False
+    for h in range(G):
+        plan = plan_hop(r, G, h, n, causal, zigzag)
+        exchanged = False
+        if h < G - 1:
+            if spare is None:
+                spare = (torch.empty_like(k), torch.empty_like(v))
+            S.comm_after_compute()
+            transport.sendrecv([(SEND, cur_k, (r + 1) % G), (SEND, cur_v, (r + 1) % G),
+                                (RECV, spare[0], (r - 1) % G), (RECV, spare[1], (r - 1) % G)],
+                               S.comm)
+            exchanged = True
+        if not plan.skip:
+            fin = h == G - 1 and plan.covers_all_queries(n)
+            kernels.fwd(plan, q, cur_k, cur_v, scale, state, o, lse, first=(h == 0), finalize=fin,
+                        stream=S.compute)
+            finalized = finalized or fin
+        if exchanged:
+            S.compute_after_comm()
+            (cur_k, cur_v), spare = spare, (cur_k, cur_v)
+            if spare[0] is k:
+                spare = None   # never receive into the caller's tensors
+    if not finalized:
+        kernels.fwd_finalize(state, o, lse, stream=S.compute)
+    return o, lse
+
+
+def _part_exchange(r: int, G: int, n: int, causal: bool, zigzag: bool, hop: int, send_bufs,
+                   kernels, like_k, like_v):
+    """Ops moving the dK/dV contribution computed at `hop` to its home rank."""
+    ops, recv_bufs = [], None
+    mine = plan_hop(r, G, hop, n, causal, zigzag)
+    if not mine.skip:
+        ops += [(SEND, send_bufs[0], mine.src), (SEND, send_bufs[1], mine.src)]
+    c = contributor_to(r, G, hop)
+    theirs = plan_hop(c, G, hop, n, causal, zigzag)
+    if not theirs.skip:
+        recv_bufs = (kernels.part(like_k), kernels.part(like_v))
+        ops += [(RECV, recv_bufs[0], c), (RECV, recv_bufs[1], c)]
+    return ops, recv_bufs
+
+
+def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: bool, transport,
+                  kernels):
+    """One rank's backward pass.  Returns (dq, dk, dv) in q's dtype."""
+    B, n, H, D = q.shape
+    G, r = transport.world, transport.rank
+    S = _Streams(q.device)
+    st = kernels.bwd_prepare(o, dout, lse, stream=S.compute)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    own = (kernels.part(k), kernels.part(v))
+    send = [None, None]
+    received = []
+    cur_k, cur_v = k, v
+    spare = None
+    for h in range(G):
+        plan = plan_hop(r, G, h, n, causal, zigzag)
+        ops = []
+        if h < G - 1:
+            if spare is None:
+                spare = (torch.empty_like(k), torch.empty_like(v))
+            ops += [(SEND, cur_k, (r + 1) % G), (SEND, cur_v, (r + 1) % G),
+                    (RECV, spare[0], (r - 1) % G), (RECV, spare[1], (r - 1) % G)]
+        if h >= 2:
+            p_ops, got = _part_exchange(r, G, n, causal, zigzag, h - 1, send[(h - 1) % 2],
+                                        kernels, k, v)
+            ops += p_ops
+            if got is not None:
+                received.append(got)
+        if ops:
+            S.comm_after_compute()
+            transport.sendrecv(ops, S.comm)
+        if h == 0:
+            target = own
+        else:
+            if send[h % 2] is None:
+                send[h % 2] = (kernels.part(k), kernels.part(v))
+            target = send[h % 2]
+        if not plan.skip:
+            kernels.bwd(plan, q, cur_k, cur_v, dout, scale, st, target[0], target[1],
+                        accumulate=False, stream=S.compute)
+        if ops:
+            S.compute_after_comm()
+        if h < G - 1:
+            (cur_k, cur_v), spare = spare, (cur_k, cur_v)
+            if spare[0] is k:
+                spare = None
+    if G > 1:
+        p_ops, got = _part_exchange(r, G, n, causal, zigzag, G - 1, send[(G - 1) % 2], kernels,
+                                    k, v)
+        if got is not None:
+            received.append(got)
+        if p_ops:
+            S.comm_after_compute()
+            transport.sendrecv(p_ops, S.comm)
+            S.compute_after_comm()
+    parts_k = [own[0]] + [x[0] for x in received]
+    parts_v = [own[1]] + [x[1] for x in received]
+    kernels.bwd_finalize(st, parts_k, parts_v, dq, dk, dv, stream=S.compute)
+    return dq, dk, dv
+
+
+def ring_comm_bytes(n_local: int, batch: int, heads: int, d: int, world: int, elem: int,
+                    causal: bool, zigzag: bool, rank: int = 0) -> tuple[int, int]:
+    """Bytes `rank` sends per forward and per backward pass (the ledger of
+    sim.py:118-153, for the K/V + fp32 dK/dV payload of this build)."""
+    kv = 2 * batch * n_local * heads * d * elem
+    part = 2 * batch * (-(-n_local // 128) * 128) * heads * d * 4
+    fwd = (world - 1) * kv
+    bwd = (world - 1) * kv
+    bwd += sum(part for h in range(1, world)
+               if not plan_hop(rank, world, h, n_local, causal, zigzag).skip)
+    return fwd, bwd
+
+
+def run_ranks(world: int, fn, timeout: float = 600.0) -> Sequence:
+    """Run fn(rank, transport) for `world` loopback ranks in threads (the
+    reference's threaded executor, sim.py:575-620); re-raise the first error."""
+    hub = LoopbackHub(world)
+    out = [None] * world
+    errors = []
+    dev = torch.cuda.current_device() if torch.cuda.is_available() else None
+
+    def work(rank):
+        try:
+            if dev is not None:
+                torch.cuda.set_device(dev)
+                s = torch.cuda.Stream()
+                with torch.cuda.stream(s):
+                    out[rank] = fn(rank, hub.transport(rank))
+                s.synchronize()
+            else:
+                out[rank] = fn(rank, hub.transport(rank))
+        except BaseException as e:  # noqa: BLE001 - surfaced below
+            errors.append(e)
+            hub.barrier.abort()
+
+    threads = [threading.Thread(target=work, args=(i,), daemon=True) for i in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout)
+    if errors:
+        raise errors[0]
+    if any(t.is_alive() for t in threads):
+        raise DeadlockError("ring ranks failed to finish")
+    return out

@@ -1,0 +1,153 @@
+"""Ring hop schedule: sequence partition, global positions and hop classes.
+
+Reference behaviour (pkg/src/burstsim):
+  * device i holds contiguous row block i (ring.partition, ring.py:97-127);
+  * at round r it holds the payload of origin (i - r) mod G (sim.py:565,
+    ring.initial_forward_body ring.py:136-145);
+  * causal = key position <= query position in GLOBAL coordinates
+    (masking.py:116-117); a fully masked hop is skipped (ring.py:169-171).
+
+B200 build (north star (4)): for causal runs the sequence is split into 2G
+chunks of c = N/(2G) and rank i holds chunks i and 2G-1-i (zigzag), so every
+rank does the same causal work.  With K/V from rank j at a hop:
+  j == i : DIAG         causal inside both chunks (global positions)
+  j <  i : K_EARLY_HALF all 2c queries x first key chunk (c keys), unmasked
+  j >  i : Q_LATE_HALF  second query chunk (c rows) x all 2c keys, unmasked
+Contiguous causal keeps the reference rule (FULL / DIAG / SKIP).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+FULL, DIAG, K_EARLY_HALF, Q_LATE_HALF, SKIP = "full", "diag", "k_early_half", "q_late_half", "skip"
+
+
+@dataclass(frozen=True)
+class PosMap:
+    """Global position of local row i: i < seg_len ? pos0 + i : pos1 + (i - seg_len)."""
+    pos0: int
+    pos1: int
+    seg_len: int
+
+    def pos(self, i: int) -> int:
+        return self.pos0 + i if i < self.seg_len else self.pos1 + (i - self.seg_len)
+
+    def positions(self, n: int) -> list[int]:
+        return [self.pos(i) for i in range(n)]
+
+
+@dataclass(frozen=True)
+class HopPlan:
+    hop: int
+    rank: int
+    src: int            # origin rank of the visiting K/V block
+    kind: str
+    q_begin: int
+    q_len: int
+    k_begin: int
+    k_len: int
+    causal: bool        # element-level causal mask inside the rectangle
+    q_map: PosMap
+    k_map: PosMap
+
+    @property
+    def skip(self) -> bool:
+        return self.kind == SKIP
+
+    def covers_all_queries(self, n_local: int) -> bool:
+        return not self.skip and self.q_begin == 0 and self.q_len == n_local
+
+
+def shard_map(rank: int, world: int, n_local: int, zigzag: bool) -> PosMap:
+    """Global positions of the rows a rank holds."""
+    if zigzag:
+        if n_local % 2:
+            raise ValueError("zigzag shards need an even local length")
+        c = n_local // 2
+        return PosMap(rank * c, (2 * world - 1 - rank) * c, c)
+    return PosMap(rank * n_local, rank * n_local + n_local, n_local)
+
+
+def source_rank(rank: int, world: int, hop: int) -> int:
+    """Origin of the K/V block a rank holds at `hop` (sim.py:565, ring.py:143)."""
+    return (rank - hop) % world
+
+
+def plan_hop(rank: int, world: int, hop: int, n_local: int, causal: bool,
+             zigzag: bool) -> HopPlan:
+    src = source_rank(rank, world, hop)
+    qm = shard_map(rank, world, n_local, zigzag)
+    km = shard_map(src, world, n_local, zigzag)
+    n = n_local
+    if not causal:
+        return HopPlan(hop, rank, src, FULL, 0, n, 0, n, False, qm, km)
+    if src == rank:
+        return HopPlan(hop, rank, src, DIAG, 0, n, 0, n, True, qm, km)
+    if zigzag:
+        c = n // 2
+        if src < rank:
+            return HopPlan(hop, rank, src, K_EARLY_HALF, 0, n, 0, c, False, qm, km)
+        return HopPlan(hop, rank, src, Q_LATE_HALF, c, c, 0, n, False, qm, km)
+    if src < rank:
+        return HopPlan(hop, rank, src, FULL, 0, n, 0, n, False, qm, km)
+    return HopPlan(hop, rank, src, SKIP, 0, 0, 0, 0, False, qm, km)
+
+
+def owner_of_contribution(rank: int, world: int, hop: int) -> int:
+    """dK/dV computed at `hop` belong to the visiting block's home rank."""
+    return source_rank(rank, world, hop)
+
+
+def contributor_to(rank: int, world: int, hop: int) -> int:
+    """Rank that computed, at `hop`, a contribution for `rank`'s own block."""
+    return (rank + hop) % world
+
+
+def hop_flops(plan: HopPlan, batch: int, heads: int, d: int) -> tuple[float, float]:
+    """Algorithmic MMA FLOPs (fwd, bwd) of one hop (sim.py:80-87 model),
+    counting only visible score entries for DIAG hops."""
+    if plan.skip:
+        return 0.0, 0.0
+    if plan.causal:
+        qp = plan.q_map.positions(plan.q_len)
+        kp = plan.k_map.positions(plan.k_len)
+        import bisect
+        ks = sorted(kp)
+        area = sum(bisect.bisect_right(ks, p) for p in qp)
+    else:
+        area = plan.q_len * plan.k_len
+    f = 4.0 * batch * heads * area * d
+    return f, 2.5 * f
+
+
+# ---------------------------------------------------------------------------
+# shard helpers (torch tensors, sequence dim = 1 for [B, N, H, D])
+# ---------------------------------------------------------------------------
+
+def shard(x, rank: int, world: int, zigzag: bool, dim: int = 1):
+    """Rows of the global tensor `x` that `rank` holds."""
+    import torch
+    n = x.shape[dim]
+    if n % (2 * world if zigzag else world):
+        raise ValueError(f"sequence length {n} not divisible for world={world} zigzag={zigzag}")
+    if not zigzag:
+        b = n // world
+        return x.narrow(dim, rank * b, b).contiguous()
+    c = n // (2 * world)
+    return torch.cat([x.narrow(dim, rank * c, c), x.narrow(dim, (2 * world - 1 - rank) * c, c)],
+                     dim=dim).contiguous()
+
+
+def unshard(parts, zigzag: bool, dim: int = 1):
+    """Inverse of `shard` given every rank's part in rank order."""
+    import torch
+    world = len(parts)
+    if not zigzag:
+        return torch.cat(list(parts), dim=dim)
+    c = parts[0].shape[dim] // 2
+    chunks = [None] * (2 * world)
+    for r, p in enumerate(parts):
+        chunks[r] = p.narrow(dim, 0, c)
+        chunks[2 * world - 1 - r] = p.narrow(dim, c, c)
+    return torch.cat(chunks, dim=dim)

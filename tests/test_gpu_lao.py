@@ -1,0 +1,85 @@
+"""GPU parity: single-device LAO (G=1) and loopback rings vs the CPU oracle.
+
+Tolerances (BASELINE.json north star): bf16 path <= 2e-2 max-abs against the
+reference's fp32 result on identical bf16-rounded inputs; fp32 path <= 1e-5
+relative (max|x-ref| / max|ref| per tensor).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from gpu_utils import make_inputs, max_abs, oracle_ring, rel_err
+
+pytestmark = pytest.mark.gpu
+
+BF16_TOL = 2e-2
+
+
+def _run(q, k, v, do, world, causal, zigzag=None):
+    from paper_2403_09347_b200 import run_ring_pass
+    res = run_ring_pass(q, k, v, world, causal=causal, dout=do, zigzag=zigzag)
+    torch.cuda.synchronize()
+    return res
+
+
+@pytest.mark.parametrize("N,D", [(256, 128), (512, 128), (384, 64), (1000, 128)])
+def test_lao_bf16_single_device(N, D):
+    q, k, v, do = make_inputs(1, N, 2, D, seed=N + D)
+    res = _run(q, k, v, do, 1, False)
+    o, lse, dq, dk, dv = oracle_ring(q, k, v, do, 1, False, False)
+    assert max_abs(res.out, o) < BF16_TOL
+    assert max_abs(res.lse, lse) < 1e-2
+    for got, ref in ((res.dq, dq), (res.dk, dk), (res.dv, dv)):
+        assert max_abs(got, ref) < BF16_TOL
+
+
+@pytest.mark.parametrize("N,D", [(256, 128), (640, 64)])
+def test_lao_bf16_causal_single_device(N, D):
+    q, k, v, do = make_inputs(2, N, 2, D, seed=7)
+    res = _run(q, k, v, do, 1, True)
+    o, lse, dq, dk, dv = oracle_ring(q, k, v, do, 1, True, False)
+    assert max_abs(res.out, o) < BF16_TOL
+    assert max_abs(res.lse, lse) < 1e-2
+    for got, ref in ((res.dq, dq), (res.dk, dk), (res.dv, dv)):
+        assert max_abs(got, ref) < BF16_TOL
+
+
+@pytest.mark.parametrize("world,causal,zigzag", [(2, False, False), (4, False, False),
+                                                 (2, True, True), (4, True, True),
+                                                 (4, True, False), (8, True, True)])
+def test_ring_bf16_loopback(world, causal, zigzag):
+    N = 256 * world * (2 if zigzag else 1)
+    q, k, v, do = make_inputs(1, N, 2, 128, seed=world)
+    res = _run(q, k, v, do, world, causal, zigzag)
+    o, lse, dq, dk, dv = oracle_ring(q, k, v, do, world, causal, zigzag)
+    assert max_abs(res.out, o) < BF16_TOL
+    assert max_abs(res.lse, lse) < 1e-2
+    for got, ref in ((res.dq, dq), (res.dk, dk), (res.dv, dv)):
+        assert max_abs(got, ref) < BF16_TOL
+
+
+@pytest.mark.parametrize("N,D,world,causal", [(512, 64, 1, False), (512, 32, 2, True),
+                                              (300, 16, 1, True)])
+def test_f32_path_rel_1e5(N, D, world, causal):
+    q, k, v, do = make_inputs(1, N, 2, D, seed=3, dtype=torch.float32)
+    res = _run(q, k, v, do, world, causal, zigzag=False)
+    o, lse, dq, dk, dv = oracle_ring(q, k, v, do, world, causal, False)
+    assert rel_err(res.out, o) < 1e-5
+    assert max_abs(res.lse, lse) < 1e-4
+    for got, ref in ((res.dq, dq), (res.dk, dk), (res.dv, dv)):
+        assert rel_err(got, ref) < 1e-5
+
+
+def test_c1_golden_fp32(golden):
+    """BASELINE configs[0] (seq 1024, d 64, 2 heads, G 2, fp32) against the
+    reference's own outputs (tests/golden, produced by the reference)."""
+    from oracle import burst_oracle as orc
+    g = golden("c1_seq1024_d64_h2_g2_f32")
+    qn, kn, vn, dn, scale = orc.generate_inputs(1024, 64, 2, 1, 0, np.float32)
+    to = lambda a: torch.from_numpy(np.ascontiguousarray(a.transpose(1, 0, 2)[None])).cuda()
+    res = _run(to(qn), to(kn), to(vn), to(dn), 2, False)
+    for key, got in (("o", res.out), ("dq", res.dq), ("dk", res.dk), ("dv", res.dv)):
+        ref = g[key].transpose(1, 0, 2)[None]
+        assert rel_err(got, ref) < 1e-5, key
+    assert rel_err(res.lse, g["lse"][None]) < 1e-5
