@@ -318,7 +318,11 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
             ops += p_ops
             if got is not None:
                 received.append(got)
-        if ops:
+        # every rank takes part in every exchange slot (a slot depends only on
+        # h and G), even with no op of its own: keeps loopback/collective
+        # transports in lockstep when causal hops are skipped
+        slot = h < G - 1 or h >= 2
+        if slot:
             S.comm_after_compute()
             transport.sendrecv(ops, S.comm)
         if h == 0:
@@ -330,7 +334,7 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
         if not plan.skip:
             kernels.bwd(plan, q, cur_k, cur_v, dout, scale, st, target[0], target[1],
                         accumulate=False, stream=S.compute)
-        if ops:
+        if slot:
             S.compute_after_comm()
         if h < G - 1:
             (cur_k, cur_v), spare = spare, (cur_k, cur_v)
@@ -341,10 +345,9 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
                                     k, v)
         if got is not None:
             received.append(got)
-        if p_ops:
-            S.comm_after_compute()
-            transport.sendrecv(p_ops, S.comm)
-            S.compute_after_comm()
+        S.comm_after_compute()
+        transport.sendrecv(p_ops, S.comm)
+        S.compute_after_comm()
     parts_k = [own[0]] + [x[0] for x in received]
     parts_v = [own[1]] + [x[1] for x in received]
     kernels.bwd_finalize(st, parts_k, parts_v, dq, dk, dv, stream=S.compute)

@@ -1,0 +1,100 @@
+"""Oracle-backed kernel provider for HOST-LOGIC tests only (CPU tensors).
+
+Implements the same interface as paper_2403_09347_b200.kernels.CudaKernels
+with the numpy oracle, so the ring engine (schedule, transports, K/V rotation,
+dK/dV routing, finalisation) can be exercised on CPU with gloo.  It is
+injected explicitly by tests; the product never imports it.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from oracle import burst_oracle as orc
+
+
+def _np(t):
+    return t.detach().double().cpu().numpy()
+
+
+class OracleKernels:
+    name = "oracle"
+
+    def __init__(self):
+        self.launches = 0
+
+    def fwd_state(self, q):
+        B, n, H, D = q.shape
+        return {"o": np.zeros((B, H, n, D)), "m": np.full((B, H, n), -np.inf),
+                "l": np.zeros((B, H, n))}
+
+    def part(self, k):
+        return torch.zeros(k.shape, dtype=torch.float64)
+
+    def fwd(self, plan, q, k, v, scale, state, o, lse, first, finalize, stream=None):
+        self.launches += 1
+        B, n, H, D = q.shape
+        qn, kn, vn = _np(q), _np(k), _np(v)
+        qp = np.array(plan.q_map.positions(n))
+        kp = np.array(plan.k_map.positions(k.shape[1]))
+        qs = slice(plan.q_begin, plan.q_begin + plan.q_len)
+        ks = slice(plan.k_begin, plan.k_begin + plan.k_len)
+        for b in range(B):
+            for h in range(H):
+                part = orc.local_forward_tiled(qn[b, qs, h], kn[b, ks, h], vn[b, ks, h], scale,
+                                               128, 128, qp[qs], kp[ks], plan.causal)
+                if first:
+                    acc = part
+                else:
+                    acc = orc.Partial(state["o"][b, h, qs].copy(), state["m"][b, h, qs].copy(),
+                                      state["l"][b, h, qs].copy())
+                    acc.merge(part)
+                if finalize:
+                    oo, ll = acc.finalize()
+                    o[b, qs, h] = torch.from_numpy(oo).to(o.dtype)
+                    lse[b, h, qs] = torch.from_numpy(ll).to(lse.dtype)
+                else:
+                    state["o"][b, h, qs], state["m"][b, h, qs], state["l"][b, h, qs] = \
+                        acc.o, acc.m, acc.l
+
+    def fwd_finalize(self, state, o, lse, stream=None):
+        self.launches += 1
+        B, n, H, D = o.shape
+        for b in range(B):
+            for h in range(H):
+                oo, ll = orc.Partial(state["o"][b, h], state["m"][b, h], state["l"][b, h]).finalize()
+                o[b, :, h] = torch.from_numpy(oo).to(o.dtype)
+                lse[b, h] = torch.from_numpy(ll).to(lse.dtype)
+
+    def bwd_prepare(self, o, dout, lse, stream=None):
+        self.launches += 1
+        d_stat = (_np(o) * _np(dout)).sum(-1).transpose(0, 2, 1)   # [B, H, n]
+        return {"lse": _np(lse), "D": d_stat, "dq": np.zeros(tuple(o.shape))}
+
+    def bwd(self, plan, q, k, v, dout, scale, st, dk_part, dv_part, accumulate, stream=None):
+        self.launches += 1
+        B, n, H, D = q.shape
+        qn, kn, vn, dn = _np(q), _np(k), _np(v), _np(dout)
+        qp = np.array(plan.q_map.positions(n))
+        kp = np.array(plan.k_map.positions(k.shape[1]))
+        qs = slice(plan.q_begin, plan.q_begin + plan.q_len)
+        ks = slice(plan.k_begin, plan.k_begin + plan.k_len)
+        if not accumulate:
+            dk_part.zero_()
+            dv_part.zero_()
+        for b in range(B):
+            for h in range(H):
+                dq, dk, dv = orc.local_backward(qn[b, qs, h], kn[b, ks, h], vn[b, ks, h],
+                                                dn[b, qs, h], st["lse"][b, h, qs],
+                                                st["D"][b, h, qs], scale, 128, 128, qp[qs],
+                                                kp[ks], plan.causal)
+                st["dq"][b, qs, h] += dq
+                dk_part[b, ks, h] += torch.from_numpy(dk)
+                dv_part[b, ks, h] += torch.from_numpy(dv)
+
+    def bwd_finalize(self, st, dk_parts, dv_parts, dq, dk, dv, stream=None):
+        self.launches += 1
+        dq.copy_(torch.from_numpy(st["dq"]).to(dq.dtype))
+        dk.copy_(sum(p for p in dk_parts).to(dk.dtype))
+        dv.copy_(sum(p for p in dv_parts).to(dv.dtype))

@@ -1,0 +1,209 @@
+"""CPU tests of the host logic: C-ABI exports, hop schedule, ring engine.
+
+The ring engine runs with an oracle-backed kernel provider (tests/oracle_kernels.py)
+over (a) the loopback transport (one thread per rank, the reference's threaded
+executor) and (b) a real 2-process torch.distributed gloo group.
+"""
+
+import os
+import re
+import subprocess
+import sys
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import burst_oracle as orc
+from oracle_kernels import OracleKernels
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "burst_b200.h")
+
+
+# ---------------------------------------------------------------- C ABI
+
+def test_library_exports_every_header_symbol():
+    from paper_2403_09347_b200 import _lib
+    declared = set(re.findall(r"BURST_API\s+[\w\s\*]+?\b(burst_\w+)\(", open(HEADER).read()))
+    assert declared, "no declarations parsed"
+    lib = _lib.load()
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert declared == set(_lib.EXPORTED)
+    assert lib.burst_version() == 1
+    assert lib.burst_workspace_floats(2, 3, 64, 130) == 2 * 3 * 256 * 64
+
+
+def test_ctypes_structs_match_c_layout():
+    from paper_2403_09347_b200 import _lib
+    import ctypes
+    src = r'''
+#include <stdio.h>
+#include <stddef.h>
+#include "burst_b200.h"
+int main(void) {
+  printf("%zu %zu %zu %zu %zu %zu\n", sizeof(burst_hop), offsetof(burst_hop, softmax_scale),
+         offsetof(burst_hop, q_map), sizeof(burst_posmap), sizeof(burst_p2p),
+         offsetof(burst_p2p, peer));
+  return 0;
+}'''
+    with tempfile.TemporaryDirectory() as d:
+        c = os.path.join(d, "t.c")
+        open(c, "w").write(src)
+        exe = os.path.join(d, "t")
+        subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), c, "-o", exe], check=True)
+        got = [int(x) for x in subprocess.run([exe], capture_output=True, text=True).stdout.split()]
+    want = [ctypes.sizeof(_lib.Hop), _lib.Hop.softmax_scale.offset, _lib.Hop.q_map.offset,
+            ctypes.sizeof(_lib.PosMap), ctypes.sizeof(_lib.P2POp), _lib.P2POp.peer.offset]
+    assert got == want
+
+
+def test_errors_map_to_reference_taxonomy():
+    from paper_2403_09347_b200 import errors
+    assert errors.CODE_TO_ERROR[1] is errors.ShapeError
+    assert errors.CODE_TO_ERROR[2] is errors.MaskError
+    assert errors.CODE_TO_ERROR[4] is errors.MissingForwardError
+    assert issubclass(errors.ShapeError, ValueError)
+
+
+def test_no_cpu_fallback():
+    from paper_2403_09347_b200 import CudaError, burst_attn_func
+    q = torch.randn(1, 8, 1, 64, dtype=torch.bfloat16)
+    with pytest.raises(CudaError):
+        burst_attn_func(q, q, q)
+
+
+# ---------------------------------------------------------------- schedule
+
+@pytest.mark.parametrize("G", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("causal,zigzag", [(False, False), (True, False), (True, True)])
+def test_hop_plans_cover_exactly_the_visible_pairs(G, causal, zigzag):
+    from paper_2403_09347_b200.schedule import plan_hop, shard_map
+    n = 8
+    N = n * G
+    visible = np.zeros((N, N), dtype=int)
+    for r in range(G):
+        for h in range(G):
+            p = plan_hop(r, G, h, n, causal, zigzag)
+            assert p.src == (r - h) % G
+            if p.skip:
+                continue
+            qp = np.array(p.q_map.positions(n))[p.q_begin:p.q_begin + p.q_len]
+            kp = np.array(p.k_map.positions(n))[p.k_begin:p.k_begin + p.k_len]
+            allowed = orc.causal_allowed(qp, kp) if p.causal else np.ones((len(qp), len(kp)), bool)
+            for i, a in enumerate(qp):
+                for j, b in enumerate(kp):
+                    if allowed[i, j]:
+                        visible[a, b] += 1
+            if not p.causal and causal:
+                assert orc.causal_allowed(qp, kp).all(), "unmasked hop must be fully visible"
+    want = orc.causal_allowed(np.arange(N), np.arange(N)) if causal else np.ones((N, N), bool)
+    assert np.array_equal(visible, want.astype(int))
+
+
+def test_zigzag_balances_work():
+    from paper_2403_09347_b200.schedule import hop_flops, plan_hop
+    G, n = 8, 256
+    work = [sum(hop_flops(plan_hop(r, G, h, n, True, True), 1, 1, 128)[0] for h in range(G))
+            for r in range(G)]
+    assert max(work) / min(work) < 1.01
+    contiguous = [sum(hop_flops(plan_hop(r, G, h, n, True, False), 1, 1, 128)[0]
+                      for h in range(G)) for r in range(G)]
+    assert max(contiguous) / min(contiguous) > 4
+
+
+def test_shard_unshard_roundtrip():
+    from paper_2403_09347_b200.schedule import shard, unshard
+    x = torch.arange(2 * 48 * 3).reshape(2, 48, 3)
+    for zz in (False, True):
+        parts = [shard(x, r, 4, zz) for r in range(4)]
+        assert torch.equal(unshard(parts, zz), x)
+
+
+# ---------------------------------------------------------------- engine
+
+def _global_reference(q, k, v, do, causal):
+    B, N, H, D = q.shape
+    outs = []
+    for b in range(B):
+        for h in range(H):
+            f = lambda t: t[b, :, h].double().numpy()
+            dq, dk, dv = orc.backward_dense(f(q), f(k), f(v), f(do), D ** -0.5, causal)
+            o, lse = orc.forward_dense(f(q), f(k), f(v), D ** -0.5, causal)
+            outs.append((b, h, o, lse, dq, dk, dv))
+    return outs
+
+
+def _check(res, q, k, v, do, causal):
+    for b, h, o, lse, dq, dk, dv in _global_reference(q, k, v, do, causal):
+        assert np.max(np.abs(res.out[b, :, h].double().numpy() - o)) < 1e-10
+        assert np.max(np.abs(res.lse[b, h].double().numpy() - lse)) < 1e-5   # lse is fp32 by contract
+        assert np.max(np.abs(res.dq[b, :, h].double().numpy() - dq)) < 1e-5
+        assert np.max(np.abs(res.dk[b, :, h].double().numpy() - dk)) < 1e-5
+        assert np.max(np.abs(res.dv[b, :, h].double().numpy() - dv)) < 1e-5
+
+
+@pytest.mark.parametrize("G,causal,zigzag", [(1, False, False), (2, False, False),
+                                             (3, False, False), (4, True, False),
+                                             (4, True, True), (2, True, True)])
+def test_engine_loopback_matches_dense(G, causal, zigzag):
+    from paper_2403_09347_b200 import run_ring_pass
+    g = torch.Generator().manual_seed(G)
+    N = 16 * G
+    q, k, v, do = (torch.randn(2, N, 2, 8, generator=g, dtype=torch.float64) for _ in range(4))
+    kern = OracleKernels()
+    res = run_ring_pass(q, k, v, G, causal=causal, dout=do, zigzag=zigzag, kernels=kern)
+    _check(res, q, k, v, do, causal)
+
+
+def _gloo_worker(rank, world, port, causal, zigzag, out_dir):
+    import torch.distributed as dist
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2403_09347_b200.api import burst_attn_func
+    from paper_2403_09347_b200.ring import TorchDistTransport
+    from paper_2403_09347_b200.schedule import shard
+    from oracle_kernels import OracleKernels as OK
+    g = torch.Generator().manual_seed(0)
+    N = 24 * world
+    q, k, v, do = (torch.randn(1, N, 2, 8, generator=g, dtype=torch.float64) for _ in range(4))
+    sh = [shard(t, rank, world, zigzag).requires_grad_(i < 3) for i, t in enumerate((q, k, v, do))]
+    o, lse = burst_attn_func(sh[0], sh[1], sh[2], causal=causal, zigzag=zigzag,
+                             _transport=TorchDistTransport(), _kernels=OK())
+    o.backward(sh[3])
+    torch.save({"o": o.detach(), "lse": lse, "dq": sh[0].grad, "dk": sh[1].grad,
+                "dv": sh[2].grad}, os.path.join(out_dir, f"r{rank}.pt"))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("causal,zigzag", [(False, False), (True, True), (True, False)])
+def test_engine_gloo_two_processes(causal, zigzag, tmp_path):
+    import socket
+    import torch.multiprocessing as mp
+    from paper_2403_09347_b200.schedule import unshard
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    world = 2
+    mp.start_processes(_gloo_worker, args=(world, port, causal, zigzag, str(tmp_path)),
+                       nprocs=world, start_method="spawn", join=True)
+    parts = [torch.load(tmp_path / f"r{r}.pt") for r in range(world)]
+
+    class R:
+        pass
+    res = R()
+    res.out = unshard([p["o"] for p in parts], zigzag, 1)
+    res.lse = unshard([p["lse"] for p in parts], zigzag, 2)
+    res.dq = unshard([p["dq"] for p in parts], zigzag, 1)
+    res.dk = unshard([p["dk"] for p in parts], zigzag, 1)
+    res.dv = unshard([p["dv"] for p in parts], zigzag, 1)
+    g = torch.Generator().manual_seed(0)
+    N = 24 * world
+    q, k, v, do = (torch.randn(1, N, 2, 8, generator=g, dtype=torch.float64) for _ in range(4))
+    _check(res, q, k, v, do, causal)
