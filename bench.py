@@ -1,0 +1,414 @@
+#!/usr/bin/env python
+"""BurstAttention forward+backward benchmark (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3|c2|c4|c5_512k]
+                    [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...       (N > 1, one rank per GPU)
+
+One step = forward + backward of attention over the whole global sequence,
+each rank holding N/G rows (contiguous shards; zigzag shards when causal) and
+the K/V (+ dK/dV) ring running over NCCL.  Prints ONE JSON line on rank 0.
+
+  value   whole-job tokens/s, device-timed (CUDA events, max over ranks),
+          inputs resident in HBM (every input tensor is 1 GiB at c3 >> 126 MB L2)
+  e2e     the same through burst_attn_func with pinned HOST buffers: H2D of
+          q/k/v/dO and D2H of out/dq/dk/dv inside the timed region
+  roofline  live per-launch timing of the dominant kernel (LAO backward) on its
+          stream; algorithmic FLOPs = 10*B*H*visible(q,k)*d per launch
+  cpu_baseline  the reference algorithm (oracle port, numpy/OpenBLAS) on a
+          bounded sample of the same workload on this host, extrapolated
+--impl reference times only that CPU path (rank 0), same metric/unit.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("attn fwd+bwd TFLOP/s/GPU & tokens/s at 128K seq, 1/2/4/8 B200; % of TC peak")
+CONFIGS = {
+    "c3": dict(workload="LLaMA-7B-shaped attention, seq 128K, 32 heads x d128, bf16, fwd+bwd, "
+                        "non-causal, ring over the N GPUs (BASELINE configs[2])",
+               seq=131072, heads=32, d=128, batch=1, causal=False),
+    "c2": dict(workload="single-GPU LAO, seq 32K, 32 heads x d128, bf16, non-causal "
+                        "(BASELINE configs[1])", seq=32768, heads=32, d=128, batch=1, causal=False),
+    "c4": dict(workload="causal LLaMA-7B-shaped attention, seq 128K, zigzag partition, bf16, "
+                        "fwd+bwd (BASELINE configs[3])", seq=131072, heads=32, d=128, batch=1,
+               causal=True),
+    "c5_512k": dict(workload="LLaMA-13B-shaped attention, 40 heads x d128, seq 512K, bf16, "
+                             "fwd+bwd (BASELINE configs[4])", seq=524288, heads=40, d=128,
+                    batch=1, causal=False),
+}
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:  # noqa: BLE001
+        return {}
+
+
+# ----------------------------------------------------------------- clocks
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.path = tempfile.mktemp(suffix=".csv")
+        self.proc = None
+        self.gpu = gpu_index
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.gpu)], stdout=open(self.path, "w"),
+                stderr=subprocess.DEVNULL)
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) >= 9 and f[1].replace(".", "").isdigit():
+                    rows.append(f)
+        except Exception:  # noqa: BLE001
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]),
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())}
+
+
+# ----------------------------------------------------------------- CPU reference
+
+def cpu_reference_sample(cfg, world: int, rows: int = 512):
+    """The reference's tiled algorithm (oracle port of local_forward_tiled +
+    local_backward, 128x128 tiles, fp32 = the reference's `single` precision)
+    on `rows` queries x all keys of one head; returns (seconds, extrapolation
+    factor to the whole global step)."""
+    import numpy as np
+    from oracle import burst_oracle as orc
+    N, d = cfg["seq"], cfg["d"]
+    rng = np.random.default_rng(0)
+    q = rng.standard_normal((rows, d), dtype=np.float32)
+    k = rng.standard_normal((N, d), dtype=np.float32)
+    v = rng.standard_normal((N, d), dtype=np.float32)
+    do = rng.standard_normal((rows, d), dtype=np.float32)
+    scale = d ** -0.5
+    qpos = np.arange(N - rows, N)     # last rows: a causal sample sees every key
+    kpos = np.arange(N)
+    t0 = time.perf_counter()
+    part = orc.local_forward_tiled(q, k, v, scale, 128, 128, qpos, kpos, cfg["causal"])
+    o, lse = part.finalize()
+    dst = (do * o).sum(1)
+    orc.local_backward(q, k, v, do, lse.astype(np.float32), dst.astype(np.float32), scale,
+                       128, 128, qpos, kpos, cfg["causal"])
+    dt = time.perf_counter() - t0
+    # whole step: batch * heads * N query rows (causal: half the pairs on average)
+    factor = cfg["batch"] * cfg["heads"] * N / rows * (0.5 if cfg["causal"] else 1.0)
+    return dt, factor
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max(i.get("num_threads", 1) for i in threadpool_info()) or 1
+    except Exception:  # noqa: BLE001
+        return os.cpu_count() or 1
+
+
+def run_reference(args, cfg, rank):
+    if rank != 0:
+        return
+    for _ in range(args.warmup):
+        cpu_reference_sample(cfg, args.gpus, args.ref_rows)
+    times = []
+    factor = 1.0
+    for _ in range(args.steps):
+        dt, factor = cpu_reference_sample(cfg, args.gpus, args.ref_rows)
+        times.append(dt)
+    t_step = statistics.mean(times) * factor
+    tokens = cfg["batch"] * cfg["seq"] / t_step
+    sample = (f"{args.ref_rows} query rows x {cfg['seq']} keys x 1 head, fwd+bwd, 128x128 tiles, "
+              f"fp32; extrapolated x{factor:.0f} to the whole step")
+    line = {"impl": "reference", "metric": METRIC, "value": tokens, "unit": "tokens/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_step * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "seq": cfg["seq"], "heads": cfg["heads"],
+                       "head_dim": cfg["d"], "batch": cfg["batch"], "causal": cfg["causal"]},
+            "cpu_baseline": {"value": tokens, "unit": "tokens/s", "cores": cpu_threads(),
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": tokens, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "tflops_per_gpu": _flops(cfg) / t_step / 1e12}
+    print(json.dumps(line), flush=True)
+
+
+def _flops(cfg):
+    f = 14.0 * cfg["batch"] * cfg["heads"] * cfg["seq"] ** 2 * cfg["d"]
+    return f / 2 if cfg["causal"] else f
+
+
+# ----------------------------------------------------------------- ours
+
+def run_ours(args, cfg, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2403_09347_b200.api import burst_attn_func
+    from paper_2403_09347_b200.kernels import CudaKernels
+    from paper_2403_09347_b200.schedule import hop_flops, plan_hop
+
+    dev = torch.device("cuda", local_rank)
+    B, N, H, D, causal = cfg["batch"], cfg["seq"], cfg["heads"], cfg["d"], cfg["causal"]
+    zigzag = causal and world > 1
+    if N % (2 * world if zigzag else world):
+        raise SystemExit(f"seq {N} not divisible for {world} ranks")
+    n = N // world
+
+    class TimedKernels(CudaKernels):
+        def __init__(self):
+            super().__init__()
+            self.on = False
+            self.launches = 0
+            self.ev = {"fwd": [], "bwd": []}
+
+        def _t(self, kind, flops, fn, stream):
+            s = stream if stream is not None else torch.cuda.current_stream()
+            if self.on:
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                fn()
+                b.record(s)
+                self.ev[kind].append((a, b, flops))
+            else:
+                fn()
+
+        def fwd(self, plan, q, k, v, scale, state, o, lse, first, finalize, stream=None):
+            self.launches += 1
+            self._t("fwd", hop_flops(plan, B, H, D)[0],
+                    lambda: super(TimedKernels, self).fwd(plan, q, k, v, scale, state, o, lse,
+                                                          first, finalize, stream), stream)
+
+        def bwd(self, plan, q, k, v, dout, scale, st, dk, dv, accumulate, stream=None):
+            self.launches += 1
+            self._t("bwd", hop_flops(plan, B, H, D)[1],
+                    lambda: super(TimedKernels, self).bwd(plan, q, k, v, dout, scale, st, dk, dv,
+                                                          accumulate, stream), stream)
+
+        def fwd_finalize(self, *a, **kw):
+            self.launches += 1
+            return super().fwd_finalize(*a, **kw)
+
+        def bwd_prepare(self, *a, **kw):
+            self.launches += 1
+            return super().bwd_prepare(*a, **kw)
+
+        def bwd_finalize(self, *a, **kw):
+            self.launches += 1
+            return super().bwd_finalize(*a, **kw)
+
+    kern = TimedKernels()
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    q, k, v, do = (torch.randn(B, n, H, D, device=dev, generator=g, dtype=torch.bfloat16)
+                   for _ in range(4))
+    for t in (q, k, v):
+        t.requires_grad_(True)
+
+    def step(qq, kk, vv, dd):
+        o, lse = burst_attn_func(qq, kk, vv, causal=causal, zigzag=zigzag, _kernels=kern)
+        grads = torch.autograd.grad(o, (qq, kk, vv), dd)
+        return o, grads
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step(q, k, v, do)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    kern.on = True
+    kern.launches = 0
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        start.record()
+        for _ in range(args.steps):
+            step(q, k, v, do)
+        end.record()
+        torch.cuda.synchronize()
+        barrier()
+    torch.cuda.synchronize()
+    kern.on = False
+    ms = start.elapsed_time(end) / args.steps
+    launches = kern.launches
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+
+    def kstats(kind):
+        ev = kern.ev[kind]
+        if not ev:
+            return None, None
+        durs = [a.elapsed_time(b) for a, b, _ in ev]
+        fl = [f for _, _, f in ev]
+        return statistics.mean(durs), statistics.mean(fl)
+
+    bwd_ms, bwd_fl = kstats("bwd")
+    fwd_ms, fwd_fl = kstats("fwd")
+
+    # ---- e2e through the public API with pinned host buffers
+    host = [t.detach().cpu().pin_memory() for t in (q, k, v, do)]
+    outs = [torch.empty(B, n, H, D, dtype=torch.bfloat16).pin_memory() for _ in range(4)]
+    dq_, dk_, dv_, do_ = (torch.empty(B, n, H, D, device=dev, dtype=torch.bfloat16)
+                          for _ in range(4))
+
+    def e2e_step():
+        qq, kk, vv = (torch.empty(B, n, H, D, device=dev, dtype=torch.bfloat16) for _ in range(3))
+        for dst, src in zip((qq, kk, vv, do_), host):
+            dst.copy_(src, non_blocking=True)
+        for t in (qq, kk, vv):
+            t.requires_grad_(True)
+        o, (gq, gk, gv) = step(qq, kk, vv, do_)
+        for dst, src in zip(outs, (o, gq, gk, gv)):
+            dst.copy_(src.detach(), non_blocking=True)
+
+    e2e_steps = max(1, min(args.steps, 3))
+    e2e_step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(e2e_steps):
+        e2e_step()
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = t.item()
+    tensor_bytes = B * n * H * D * 2
+
+    if rank != 0:
+        return
+    peaks = _peaks()
+    peak_burst = peaks.get("bf16_tflops", 1590.0)
+    peak_sus = peaks.get("bf16_tflops_sustained", 1400.0)
+    peak_src = "MEASURED_PEAKS.json" if peaks else "fallback (B200_PROFILING.md)"
+    tokens = B * N / (ms / 1e3)
+    tflops_gpu = _flops(cfg) / world / (ms / 1e3) / 1e12
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = tr.get(f"{args.config}_g{world}", {}).get("lao_bwd")
+    except Exception:  # noqa: BLE001
+        pass
+    roof = None
+    if bwd_ms:
+        ach = bwd_fl / (bwd_ms / 1e3) / 1e12
+        roof = {"bound": "tensor", "kernel": "lao_bwd_kernel<128> (LAO backward, sm_100a tcgen05)",
+                "achieved": ach, "peak": peak_sus, "unit": "TFLOP/s", "frac": ach / peak_sus,
+                "peak_kind": f"bf16 sustained ({peak_src}); kernel runs inside a long step",
+                "frac_of_burst_peak": ach / peak_burst, "traffic": traffic,
+                "flops_per_launch": bwd_fl, "ms_per_launch": bwd_ms}
+        if fwd_ms:
+            fa = fwd_fl / (fwd_ms / 1e3) / 1e12
+            roof["lao_fwd"] = {"achieved": fa, "frac": fa / peak_sus,
+                               "frac_of_burst_peak": fa / peak_burst, "ms_per_launch": fwd_ms,
+                               "flops_per_launch": fwd_fl}
+    cpu = None
+    if world == 1 and not args.skip_cpu:
+        dt, factor = cpu_reference_sample(cfg, 1, args.ref_rows)
+        ct = dt * factor
+        cpu = {"value": B * N / ct, "unit": "tokens/s", "cores": cpu_threads(), "kind": "port",
+               "sample": f"{args.ref_rows} query rows x {N} keys x 1 head fwd+bwd (reference "
+                         f"tiled algorithm, numpy fp32) in {dt:.2f}s, extrapolated x{factor:.0f}",
+               "tflops": _flops(cfg) / ct / 1e12}
+    comm = None
+    if world > 1:
+        from paper_2403_09347_b200.ring import ring_comm_bytes
+        fb, bb = ring_comm_bytes(n, B, H, D, world, 2, causal, zigzag)
+        comm = {"bytes_sent_per_rank_per_step": fb + bb,
+                "avg_GBps_over_step": (fb + bb) / (ms / 1e3) / 1e9}
+    line = {
+        "metric": METRIC, "value": tokens, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded N(0,1) q/k/v/dO)",
+        "config": {"workload": cfg["workload"], "seq": N, "heads": H, "head_dim": D, "batch": B,
+                   "causal": causal, "partition": "zigzag" if zigzag else "contiguous",
+                   "parallelism": f"ring sp{world}", "l2": "inputs larger than L2 "
+                   f"({tensor_bytes / 2**30:.2f} GiB per tensor per rank)"},
+        "tflops_per_gpu": tflops_gpu, "tc_peak_frac": tflops_gpu / peak_sus,
+        "tc_peak_frac_of_burst": tflops_gpu / peak_burst,
+        "e2e": {"value": B * N / (e2e_ms / 1e3), "unit": "tokens/s",
+                "h2d_bytes_per_step": 4 * tensor_bytes, "d2h_bytes_per_step": 4 * tensor_bytes,
+                "ms_per_step": e2e_ms, "api": "burst_attn_func + autograd (pinned host buffers)"},
+        "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(),
+        "gpu_launches": launches, "comm": comm,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-rows", type=int, default=512)
+    ap.add_argument("--skip-cpu", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, cfg, rank)
+        return
+    import torch
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.gpus != world and world > 1:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    run_ours(args, cfg, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
