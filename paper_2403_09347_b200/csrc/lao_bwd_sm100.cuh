@@ -15,8 +15,8 @@
 //   warps 4-7  dQ drain warpgroup (thread = query row of the dQ tile)
 //   warp  8    TMA producer (+ TMEM allocator)
 //   warp  9    tcgen05.mma issuer
-// TMEM (512 cols for D=128): S^T [0,128) (P^T bf16 in [0,64), then dQ_i),
-// dP^T [128,256), dV [256,256+D), dK [256+D,256+2D).
+// TMEM (512 cols for D=128): S^T [0,128) (P^T bf16 in [0,64)), dP^T [128,256)
+// (then dQ_i once dS_i is built), dV [256,256+D), dK [256+D,256+2D).
 #pragma once
 #include <cuda.h>
 #include "common.cuh"
@@ -91,7 +91,8 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_const
   uint64_t* dq_full = bars + 9;
   uint64_t* dq_empty = bars + 10;
   uint64_t* dkv_full = bars + 11;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* dp_full = bars + 12;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 13);
 
   const burst_hop& hp = p.hop;
   const int warp = threadIdx.x >> 5;
@@ -126,6 +127,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_const
       ptx::mbar_init(dq_full, 1);
       ptx::mbar_init(dq_empty, BM);
       ptx::mbar_init(dkv_full, 1);
+      ptx::mbar_init(dp_full, 1);
       ptx::fence_mbar_init();
       ptx::tma_prefetch_desc(&p.tm_q);
       ptx::tma_prefetch_desc(&p.tm_k);
@@ -169,37 +171,43 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_const
     }
   } else if (warp == 9) {
     // ------------------------------------------------------------ MMA issuer
+    // Order per query tile i (steady state):
+    //   dV_i | S^T_{i+1} (overlaps dS_i) | dK_i, dQ_i -> dP region | dP^T_{i+1} (after dQ_i drained)
     if (lane == 0 && nq > 0) {
       constexpr uint32_t id_kk = ptx::make_idesc_bf16(BN, BM, 0, 0);   // S^T, dP^T
       constexpr uint32_t id_kmn = ptx::make_idesc_bf16(BN, D, 0, 1);   // dV, dK (B MN-major)
       constexpr uint32_t id_mnmn = ptx::make_idesc_bf16(BM, D, 1, 1);  // dQ (A, B MN-major)
       const uint32_t aK = ptx::smem_u32(sK), aV = ptx::smem_u32(sV);
       const uint32_t aQ = ptx::smem_u32(sQ), adO = ptx::smem_u32(sdO), adS = ptx::smem_u32(sdS);
-      ptx::mbar_wait(kv_full, 0);
-      for (int i = 0; i < nq; ++i) {
-        const int s = i & 1;
-        const uint32_t q = aQ + s * C::kTileBytes, dO = adO + s * C::kTileBytes;
-        ptx::mbar_wait(qdo_full + s, (i >> 1) & 1);
-        ptx::tc_fence_after();
-        // dP^T = V dO^T   (K-major both, reduction over D)
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * C::kBoxBytes + (kk & 3) * 32;
-          ptx::mma_ss(tbase + kDP, ptx::make_sdesc(aV + off, 0, 1024),
-                      ptx::make_sdesc(dO + off, 0, 1024), id_kk, kk > 0);
-        }
-        if (i > 0) {
-          ptx::mbar_wait(dq_empty, (i - 1) & 1);
-          ptx::tc_fence_after();
-        }
-        // S^T = K Q^T
+      auto st_mma = [&](int stage) {   // S^T = K Q^T
+        const uint32_t q = aQ + stage * C::kTileBytes;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * C::kBoxBytes + (kk & 3) * 32;
           ptx::mma_ss(tbase + kS, ptx::make_sdesc(aK + off, 0, 1024),
                       ptx::make_sdesc(q + off, 0, 1024), id_kk, kk > 0);
         }
-        ptx::mma_commit(s_full);
+      };
+      auto dpt_mma = [&](int stage) {  // dP^T = V dO^T
+        const uint32_t dO = adO + stage * C::kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * C::kBoxBytes + (kk & 3) * 32;
+          ptx::mma_ss(tbase + kDP, ptx::make_sdesc(aV + off, 0, 1024),
+                      ptx::make_sdesc(dO + off, 0, 1024), id_kk, kk > 0);
+        }
+      };
+      ptx::mbar_wait(kv_full, 0);
+      ptx::mbar_wait(qdo_full + 0, 0);
+      ptx::tc_fence_after();
+      st_mma(0);
+      ptx::mma_commit(s_full);
+      dpt_mma(0);
+      ptx::mma_commit(dp_full);
+      for (int i = 0; i < nq; ++i) {
+        const int s = i & 1;
+        const bool more = i + 1 < nq;
+        const uint32_t q = aQ + s * C::kTileBytes, dO = adO + s * C::kTileBytes;
         // dV += P^T dO   (A = P^T from TMEM, B = dO MN-major, reduction over queries)
         ptx::mbar_wait(p_full, i & 1);
         ptx::tc_fence_after();
@@ -208,7 +216,13 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_const
           ptx::mma_ts(tbase + kDV, tbase + kS + kk * 8,
                       ptx::make_sdesc(dO + kk * 2048, C::kBoxBytes, 1024), id_kmn,
                       (i > 0 || kk > 0) ? 1u : 0u);
-        // dK += dS^T Q ; dQ_i = dS K
+        if (more) {
+          ptx::mbar_wait(qdo_full + (s ^ 1), ((i + 1) >> 1) & 1);
+          ptx::tc_fence_after();
+          st_mma(s ^ 1);
+          ptx::mma_commit(s_full);
+        }
+        // dK += dS^T Q ; dQ_i = dS K  (into the dP^T columns, already consumed)
         ptx::mbar_wait(ds_full, i & 1);
         ptx::tc_fence_after();
 #pragma unroll
@@ -220,11 +234,17 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_const
         }
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk)
-          ptx::mma_ss(tbase + kS, ptx::make_sdesc(adS + kk * 2048, 16384, 1024),
+          ptx::mma_ss(tbase + kDP, ptx::make_sdesc(adS + kk * 2048, 16384, 1024),
                       ptx::make_sdesc(aK + kk * 2048, C::kBoxBytes, 1024), id_mnmn, kk > 0);
         ptx::mma_commit(dq_full);
         ptx::mma_commit(ds_empty);
         ptx::mma_commit(qdo_empty + s);
+        if (more) {
+          ptx::mbar_wait(dq_empty, i & 1);
+          ptx::tc_fence_after();
+          dpt_mma(s ^ 1);
+          ptx::mma_commit(dp_full);
+        }
       }
       ptx::mma_commit(dkv_full);
     }
@@ -243,27 +263,36 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_const
       const int s = i & 1;
       const int64_t q0 = qs + (int64_t)i * BM;
       // visible query columns of this key row: [lo, hi)
-      int64_t lo = qfirst - q0, hi = q_end - q0;
-      if (lo < 0) lo = 0;
-      if (hi > BM) hi = BM;
-      if (!kvalid) hi = 0;
+      int64_t lo64 = qfirst - q0, hi64 = q_end - q0;
+      const int lo = lo64 < 0 ? 0 : (lo64 > BM ? BM : (int)lo64);
+      const int hi = !kvalid ? 0 : (hi64 > BM ? BM : (hi64 < 0 ? 0 : (int)hi64));
+      const bool warp_full = __all_sync(0xffffffffu, lo == 0 && hi == BM);
       ptx::mbar_wait(qdo_full + s, (i >> 1) & 1);
       ptx::mbar_wait(s_full, i & 1);
       ptx::tc_fence_after();
-      const float* lse2 = sStat + s * 2 * BM;
-      const float* dst = lse2 + BM;
+      const float4* lse4 = reinterpret_cast<const float4*>(sStat + s * 2 * BM);
+      const float4* dst4 = lse4 + BM / 4;
       float pr[BM];
+      {
+        uint32_t r[BM];
 #pragma unroll
-      for (int cc = 0; cc < BM / 32; ++cc) {
-        uint32_t r[32];
-        ptx::tmem_ld32(tbase + lane_off + kS + cc * 32, r);
+        for (int cc = 0; cc < BM / 32; ++cc)
+          ptx::tmem_ld32(tbase + lane_off + kS + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(r + cc * 32));
         ptx::tmem_wait_ld();
+        ptx::reg_fence(r);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int c = cc * 32 + j;
-          const float e = ptx::ex2(fmaf(__uint_as_float(r[j]), c2, -lse2[c]));
-          pr[c] = (c >= lo && c < hi) ? e : 0.f;
+        for (int c4 = 0; c4 < BM / 4; ++c4) {
+          const float4 L = lse4[c4];
+          pr[4 * c4 + 0] = ptx::ex2(fmaf(__uint_as_float(r[4 * c4 + 0]), c2, -L.x));
+          pr[4 * c4 + 1] = ptx::ex2(fmaf(__uint_as_float(r[4 * c4 + 1]), c2, -L.y));
+          pr[4 * c4 + 2] = ptx::ex2(fmaf(__uint_as_float(r[4 * c4 + 2]), c2, -L.z));
+          pr[4 * c4 + 3] = ptx::ex2(fmaf(__uint_as_float(r[4 * c4 + 3]), c2, -L.w));
         }
+      }
+      if (!warp_full) {
+#pragma unroll
+        for (int c = 0; c < BM; ++c)
+          if (c < lo || c >= hi) pr[c] = 0.f;
       }
 #pragma unroll
       for (int cc = 0; cc < BM / 64; ++cc) {
@@ -276,28 +305,32 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_const
       ptx::tc_fence_before();
       ptx::mbar_arrive(p_full);
 
+      ptx::mbar_wait(dp_full, i & 1);
       ptx::mbar_wait(ds_empty, (i & 1) ^ 1);
+      ptx::tc_fence_after();
 #pragma unroll
-      for (int cc = 0; cc < BM / 32; ++cc) {
-        uint32_t r[32];
-        ptx::tmem_ld32(tbase + lane_off + kDP + cc * 32, r);
+      for (int half = 0; half < 2; ++half) {
+        uint32_t r[64];
+        ptx::tmem_ld32(tbase + lane_off + kDP + half * 64, *reinterpret_cast<uint32_t(*)[32]>(r));
+        ptx::tmem_ld32(tbase + lane_off + kDP + half * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
         ptx::tmem_wait_ld();
-        uint32_t pk[16];
+        ptx::reg_fence(r);
+        uint32_t pk[32];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int c = cc * 32 + 2 * j;
-          const float d0 = pr[c] * (__uint_as_float(r[2 * j]) - dst[c]);
-          const float d1 = pr[c + 1] * (__uint_as_float(r[2 * j + 1]) - dst[c + 1]);
-          pk[j] = ptx::pack_bf16(d0, d1);
+        for (int j4 = 0; j4 < 16; ++j4) {
+          const float4 Dv = dst4[half * 16 + j4];
+          const int c = half * 64 + 4 * j4;
+          pk[2 * j4] = ptx::pack_bf16(pr[c] * (__uint_as_float(r[4 * j4]) - Dv.x),
+                                      pr[c + 1] * (__uint_as_float(r[4 * j4 + 1]) - Dv.y));
+          pk[2 * j4 + 1] = ptx::pack_bf16(pr[c + 2] * (__uint_as_float(r[4 * j4 + 2]) - Dv.z),
+                                          pr[c + 3] * (__uint_as_float(r[4 * j4 + 3]) - Dv.w));
         }
-        // SW128 K-major: row t, query chunk (16 B = 8 bf16) index ch in [0,8) of half x
-        uint8_t* rowp = sdS + (cc >> 1) * 16384 + t * 128;
+        // SW128 K-major: row t, 16-byte query chunk ch (8 bf16) of 128 B swizzle row
+        uint8_t* rowp = sdS + half * 16384 + t * 128;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int ch = (cc & 1) * 4 + u;
+        for (int ch = 0; ch < 8; ++ch)
           *reinterpret_cast<uint4*>(rowp + ((ch ^ (t & 7)) << 4)) =
-              make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
-        }
+              make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
       }
       ptx::fence_proxy_async_smem();
       ptx::tc_fence_before();
@@ -319,6 +352,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_const
         if (nq > 0) {
           ptx::tmem_ld32(tbase + lane_off + col0 + cc * 32, r);
           ptx::tmem_wait_ld();
+          ptx::reg_fence(r);
         } else {
 #pragma unroll
           for (int j = 0; j < 32; ++j) r[j] = 0u;
@@ -346,22 +380,21 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_const
       const bool qvalid = qrow < q_end && qrow < hp.n_q;
       ptx::mbar_wait(dq_full, i & 1);
       ptx::tc_fence_after();
+      uint32_t r[D];
 #pragma unroll
-      for (int cc = 0; cc < D / 32; ++cc) {
-        uint32_t r[32];
-        ptx::tmem_ld32(tbase + lane_off + kS + cc * 32, r);
-        ptx::tmem_wait_ld();
-        if (cc == D / 32 - 1) {
-          ptx::tc_fence_before();
-          ptx::mbar_arrive(dq_empty);
-        }
-        if (qvalid) {
+      for (int cc = 0; cc < D / 32; ++cc)
+        ptx::tmem_ld32(tbase + lane_off + kDP + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(r + cc * 32));
+      ptx::tmem_wait_ld();
+      ptx::reg_fence(r);
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(dq_empty);
+      if (qvalid) {
+        float* base = p.dq_acc + tl_index(bh, qrow, 0, D, NTq);
 #pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            ptx::red_add_v4(p.dq_acc + tl_index(bh, qrow, cc * 32 + j, D, NTq),
-                            __uint_as_float(r[j]) * p.scale, __uint_as_float(r[j + 1]) * p.scale,
-                            __uint_as_float(r[j + 2]) * p.scale, __uint_as_float(r[j + 3]) * p.scale);
-        }
+        for (int j = 0; j < D; j += 4)   // next 4-column group: 128 rows x 4 floats further
+          ptx::red_add_v4(base + (size_t)(j >> 2) * 512, __uint_as_float(r[j]) * p.scale,
+                          __uint_as_float(r[j + 1]) * p.scale, __uint_as_float(r[j + 2]) * p.scale,
+                          __uint_as_float(r[j + 3]) * p.scale);
       }
     }
   }

@@ -227,14 +227,16 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
       ptx::mbar_wait(s_full + g, j & 1);
       ptx::tc_fence_after();
       float s[BN];
+      {
+        uint32_t r[BN];
 #pragma unroll
-      for (int cc = 0; cc < BN / 32; ++cc) {
-        uint32_t r[32];
-        ptx::tmem_ld32(tS + cc * 32, r);
+        for (int cc = 0; cc < BN / 32; ++cc)
+          ptx::tmem_ld32(tS + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(r + cc * 32));
+        ptx::tmem_wait_ld();
+        ptx::reg_fence(r);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) s[cc * 32 + i] = __uint_as_float(r[i]);
+        for (int i = 0; i < BN; ++i) s[i] = __uint_as_float(r[i]);
       }
-      ptx::tmem_wait_ld();
       const int64_t nvalid = lim - (int64_t)j * BN;
       if (__any_sync(0xffffffffu, nvalid < BN)) {
 #pragma unroll
