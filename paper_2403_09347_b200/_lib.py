@@ -13,7 +13,8 @@ import threading
 
 from .errors import CODE_TO_ERROR, CudaError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libburst_b200.so")
+LIB_PATH = os.environ.get("BURST_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                        "libburst_b200.so")
 
 DTYPE_BF16 = 0
 DTYPE_F32 = 1

@@ -112,6 +112,11 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_const
     if (first_q > qs) qs = hp.q_begin + ((first_q - hp.q_begin) / BM) * BM;
   }
   const int nq = qs < q_end ? (int)ceil_div(q_end - qs, BM) : 0;
+  // Query-tile visiting order is rotated per CTA: concurrently resident CTAs (consecutive
+  // key tiles of one head) then reduce into different dQ tiles instead of all hitting
+  // the same 64 KB of dQ_acc at once (L2 atomic hot spot).
+  const int rot = nq > 0 ? (int)((blockIdx.x * 7u) % (unsigned)nq) : 0;
+  auto qtile = [&](int i) -> int64_t { int j = i + rot; if (j >= nq) j -= nq; return qs + (int64_t)j * BM; };
 
   if (warp == 8) {
     if (lane == 0) {
@@ -143,7 +148,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_const
   const uint32_t tbase = *tmem_holder;
   constexpr uint32_t kS = 0, kDP = 128, kDV = 256, kDK = 256 + D;
   if (warp >= 8) {
-   ptx::regs_dec<56>();
+   ptx::regs_dec<88>();
    if (warp == 8) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0 && nq > 0) {
@@ -154,7 +159,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_const
       }
       for (int i = 0; i < nq; ++i) {
         const int s = i & 1;
-        const int64_t q0 = qs + (int64_t)i * BM;
+        const int64_t q0 = qtile(i);
         ptx::mbar_wait(qdo_empty + s, ((i >> 1) & 1) ^ 1);
         ptx::mbar_expect_tx(qdo_full + s, 2 * C::kTileBytes + C::kStatBytes);
         for (int x = 0; x < C::kBoxes; ++x) {
@@ -261,7 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_const
     const float c2 = p.scale_log2;
     for (int i = 0; i < nq; ++i) {
       const int s = i & 1;
-      const int64_t q0 = qs + (int64_t)i * BM;
+      const int64_t q0 = qtile(i);
       // visible query columns of this key row: [lo, hi)
       int64_t lo64 = qfirst - q0, hi64 = q_end - q0;
       const int lo = lo64 < 0 ? 0 : (lo64 > BM ? BM : (int)lo64);
@@ -376,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_const
     const int t = threadIdx.x & 127;           // query row within the tile
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     for (int i = 0; i < nq; ++i) {
-      const int64_t qrow = qs + (int64_t)i * BM + t;
+      const int64_t qrow = qtile(i) + t;
       const bool qvalid = qrow < q_end && qrow < hp.n_q;
       ptx::mbar_wait(dq_full, i & 1);
       ptx::tc_fence_after();

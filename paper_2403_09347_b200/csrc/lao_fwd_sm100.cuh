@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
   ptx::tc_fence_after();
   const uint32_t tbase = *tmem_holder;
   if (warp >= 8) {
-   ptx::regs_dec<56>();
+   ptx::regs_dec<88>();
    if (warp == 8) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0 && nkv > 0) {
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
    }
   } else {
     // ------------------------------------------------------------ softmax WGs
-    ptx::regs_inc<224>();
+    ptx::regs_inc<208>();
     const int g = warp >> 2;                 // query tile 0/1
     const int t = threadIdx.x & 127;         // row within the tile = TMEM lane
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
@@ -243,9 +243,14 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
         for (int i = 0; i < BN; ++i)
           if (i >= nvalid) s[i] = -INFINITY;
       }
-      float mx = s[0];
+      // row max as 8 independent chains (a single chain is 128 dependent FMNMX)
+      float mx8[8];
 #pragma unroll
-      for (int i = 1; i < BN; ++i) mx = fmaxf(mx, s[i]);
+      for (int u = 0; u < 8; ++u) mx8[u] = s[u];
+#pragma unroll
+      for (int i = 8; i < BN; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
+      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
       const float m_tile = mx * c2;
       const bool grow = m_tile > m_run + kRescaleThreshold || (m_run == -INFINITY && m_tile > -INFINITY);
       if (__any_sync(0xffffffffu, grow && j > 0)) {
@@ -266,7 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
         m_run = fmaxf(m_tile, m_run);
       }
       const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-      float lsum = 0.f;
+      float ls8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int cc = 0; cc < BN / 64; ++cc) {
         uint32_t pk[32];
@@ -274,12 +279,13 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
         for (int i = 0; i < 32; ++i) {
           const float p0 = ptx::ex2(fmaf(s[cc * 64 + 2 * i], c2, -m_use));
           const float p1 = ptx::ex2(fmaf(s[cc * 64 + 2 * i + 1], c2, -m_use));
-          lsum += p0 + p1;
+          ls8[(2 * i) & 7] += p0;
+          ls8[(2 * i + 1) & 7] += p1;
           pk[i] = ptx::pack_bf16(p0, p1);
         }
         ptx::tmem_st32(tS + cc * 32, pk);
       }
-      l_run += lsum;
+      l_run += ((ls8[0] + ls8[1]) + (ls8[2] + ls8[3])) + ((ls8[4] + ls8[5]) + (ls8[6] + ls8[7]));
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
       ptx::mbar_arrive(p_full + g);

@@ -205,15 +205,22 @@ __device__ __forceinline__ void regs_dec() {
 
 // ---------------------------------------------------------------- math
 __device__ __forceinline__ float ex2(float x) {
+#ifdef BURST_EXP_CHEAP_EXP   // timing experiment only: removes MUFU from the critical path
+  return fmaf(x, 0.01f, 1.0f);
+#else
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+#endif
 }
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
 __device__ __forceinline__ void red_add_v4(float* gaddr, float a, float b, float c, float d) {
+#ifdef BURST_EXP_NO_DQ_RED   // timing experiment only: drops the dQ reduction traffic
+  return;
+#endif
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(gaddr), "f"(a), "f"(b),
                "f"(c), "f"(d)
                : "memory");
