@@ -46,7 +46,7 @@ def oracle_ring(q, k, v, do, world, causal, zigzag, scale=None, tile=128, with_g
 
 
 def max_abs(a, b):
-    a = a.float().cpu().numpy() if isinstance(a, torch.Tensor) else a
+    a = a.detach().float().cpu().numpy() if isinstance(a, torch.Tensor) else a
     return float(np.max(np.abs(np.asarray(a, np.float64) - np.asarray(b, np.float64))))
 
 
