@@ -5,12 +5,14 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
 
 #include "../../include/burst_b200.h"
 #include "aux_kernels.cuh"
+#include "lao_bwd2_sm100.cuh"
 #include "lao_bwd_sm100.cuh"
 #include "lao_fwd_sm100.cuh"
 #include "simt_f32.cuh"
@@ -52,14 +54,15 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // 4-D map over a [B, n, H, D] bf16 tensor; box = 64 columns x 1 head x 128 rows.
-int make_tmap(CUtensorMap* tm, const void* base, int64_t n, int H, int D, int B) {
+int make_tmap(CUtensorMap* tm, const void* base, int64_t n, int H, int D, int B,
+              int box_rows = 128) {
   auto fn = encode_fn();
   if (!fn) return fail(BURST_E_CUDA, "cuTensorMapEncodeTiled unavailable");
   if ((reinterpret_cast<uintptr_t>(base) & 15) != 0)
     return fail(BURST_E_SHAPE, "tensor base must be 16-byte aligned");
   cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)H, (cuuint64_t)n, (cuuint64_t)B};
   cuuint64_t strides[3] = {(cuuint64_t)D * 2, (cuuint64_t)H * D * 2, (cuuint64_t)n * H * D * 2};
-  cuuint32_t box[4] = {64, 1, 128, 1};
+  cuuint32_t box[4] = {64, 1, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -184,6 +187,41 @@ int launch_bwd_bf16(const burst_hop* h, const void* q, const void* k, const void
   return BURST_OK;
 }
 
+// CTA-pair backward (cta_group::2, 256 keys per pair): half the dQ reduction volume.
+int launch_bwd2_bf16(const burst_hop* h, const void* q, const void* k, const void* v, const void* dout,
+                     const float* stats, float* dq_acc, float* dk, float* dv, int acc, cudaStream_t st) {
+  bwd2::Params p;
+  memset(&p, 0, sizeof(p));
+  int rc;
+  if ((rc = make_tmap(&p.tm_q128, q, h->n_q, h->heads, 128, h->batch))) return rc;
+  if ((rc = make_tmap(&p.tm_q64, q, h->n_q, h->heads, 128, h->batch, 64))) return rc;
+  if ((rc = make_tmap(&p.tm_do128, dout, h->n_q, h->heads, 128, h->batch))) return rc;
+  if ((rc = make_tmap(&p.tm_do64, dout, h->n_q, h->heads, 128, h->batch, 64))) return rc;
+  if ((rc = make_tmap(&p.tm_k, k, h->n_k, h->heads, 128, h->batch))) return rc;
+  if ((rc = make_tmap(&p.tm_v, v, h->n_k, h->heads, 128, h->batch))) return rc;
+  p.stats = stats; p.dq_acc = dq_acc; p.dk_acc = dk; p.dv_acc = dv;
+  p.hop = *h;
+  p.scale_log2 = h->softmax_scale * kLog2e;
+  p.scale = h->softmax_scale;
+  p.accumulate = acc;
+  static std::once_flag once;
+  static int attr_rc = 0;
+  std::call_once(once, [] { attr_rc = set_smem(bwd2::lao_bwd2_kernel, bwd2::kSmemBytes); });
+  if (attr_rc) return attr_rc;
+  dim3 grid((unsigned)(2 * ceil_div(h->k_len, 2 * bwd2::BN)), h->heads, h->batch);
+  bwd2::lao_bwd2_kernel<<<grid, bwd2::kThreads, bwd2::kSmemBytes, st>>>(p);
+  CHECK_LAUNCH();
+  return BURST_OK;
+}
+
+bool use_pair_bwd() {
+  static int v = [] {
+    const char* e = getenv("BURST_BWD_KERNEL");   // "1": single-CTA kernel (A/B timing)
+    return (e && e[0] == '1') ? 0 : 1;
+  }();
+  return v != 0;
+}
+
 template <int D>
 int launch_bwd_f32(const burst_hop* h, const void* q, const void* k, const void* v, const void* dout,
                    const float* stats, float* dq_acc, float* dk, float* dv, int acc, cudaStream_t st) {
@@ -301,7 +339,11 @@ int burst_lao_bwd(const burst_hop* hop, const void* q, const void* k, const void
   if (hop->k_len == 0) return BURST_OK;
   cudaStream_t st = (cudaStream_t)stream;
   if (hop->dtype == BURST_DTYPE_BF16) {
-    if (hop->head_dim == 128) return launch_bwd_bf16<128>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
+    if (hop->head_dim == 128) {
+      if (use_pair_bwd())
+        return launch_bwd2_bf16(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
+      return launch_bwd_bf16<128>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
+    }
     return launch_bwd_bf16<64>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
   }
   switch (hop->head_dim) {
