@@ -13,6 +13,7 @@
 #include "../../include/burst_b200.h"
 #include "aux_kernels.cuh"
 #include "lao_bwd2_sm100.cuh"
+#include "lao_bwd3_sm100.cuh"
 #include "lao_bwd_sm100.cuh"
 #include "lao_fwd_sm100.cuh"
 #include "simt_f32.cuh"
@@ -83,6 +84,14 @@ int* device_flags() {
   }
   return flags[dev];
 }
+
+#ifdef BURST_TRACE
+long long* trace_buffer() {
+  static long long* buf = nullptr;
+  if (!buf) { cudaMalloc(&buf, 32 * 64 * sizeof(long long)); cudaMemset(buf, 0, 32 * 64 * sizeof(long long)); }
+  return buf;
+}
+#endif
 
 bool valid_map(const burst_posmap& m) { return m.seg_len >= 0 && m.pos0 + m.seg_len <= m.pos1; }
 
@@ -177,6 +186,9 @@ int launch_bwd_bf16(const burst_hop* h, const void* q, const void* k, const void
   p.scale_log2 = h->softmax_scale * kLog2e;
   p.scale = h->softmax_scale;
   p.accumulate = acc;
+#ifdef BURST_TRACE
+  p.trace = trace_buffer();
+#endif
   static std::once_flag once;
   static int attr_rc = 0;
   std::call_once(once, [] { attr_rc = set_smem(bwd::lao_bwd_kernel<D>, bwd::Cfg<D>::kSmemBytes); });
@@ -214,12 +226,39 @@ int launch_bwd2_bf16(const burst_hop* h, const void* q, const void* k, const voi
   return BURST_OK;
 }
 
-bool use_pair_bwd() {
+// Backward kernel variant for bf16 (BURST_BWD_KERNEL: 1 = single CTA + red.global,
+// 2 = CTA pair, 3 = single CTA + SMEM-staged TMA bulk reductions; default 3).
+int bwd_variant() {
   static int v = [] {
-    const char* e = getenv("BURST_BWD_KERNEL");   // "1": single-CTA kernel (A/B timing)
-    return (e && e[0] == '1') ? 0 : 1;
+    const char* e = getenv("BURST_BWD_KERNEL");
+    return (e && e[0] >= '1' && e[0] <= '3') ? e[0] - '0' : 3;
   }();
-  return v != 0;
+  return v;
+}
+
+template <int D>
+int launch_bwd3_bf16(const burst_hop* h, const void* q, const void* k, const void* v, const void* dout,
+                     const float* stats, float* dq_acc, float* dk, float* dv, int acc, cudaStream_t st) {
+  bwd3::Params p;
+  memset(&p, 0, sizeof(p));
+  int rc;
+  if ((rc = make_tmap(&p.tm_q, q, h->n_q, h->heads, D, h->batch))) return rc;
+  if ((rc = make_tmap(&p.tm_do, dout, h->n_q, h->heads, D, h->batch))) return rc;
+  if ((rc = make_tmap(&p.tm_k, k, h->n_k, h->heads, D, h->batch))) return rc;
+  if ((rc = make_tmap(&p.tm_v, v, h->n_k, h->heads, D, h->batch))) return rc;
+  p.stats = stats; p.dq_acc = dq_acc; p.dk_acc = dk; p.dv_acc = dv;
+  p.hop = *h;
+  p.scale_log2 = h->softmax_scale * kLog2e;
+  p.scale = h->softmax_scale;
+  p.accumulate = acc;
+  static std::once_flag once;
+  static int attr_rc = 0;
+  std::call_once(once, [] { attr_rc = set_smem(bwd3::lao_bwd3_kernel<D>, bwd3::Cfg<D>::kSmemBytes); });
+  if (attr_rc) return attr_rc;
+  dim3 grid((unsigned)ceil_div(h->k_len, bwd3::BN), h->heads, h->batch);
+  bwd3::lao_bwd3_kernel<D><<<grid, bwd3::kThreads, bwd3::Cfg<D>::kSmemBytes, st>>>(p);
+  CHECK_LAUNCH();
+  return BURST_OK;
 }
 
 template <int D>
@@ -259,6 +298,13 @@ int check_dims(int dtype, int B, int H, int D, int64_t n) {
 }
 
 }  // namespace
+
+#ifdef BURST_TRACE
+extern "C" __attribute__((visibility("default"))) int burst_exp_trace_read(long long* host) {
+  cudaDeviceSynchronize();
+  return (int)cudaMemcpy(host, trace_buffer(), 32 * 64 * sizeof(long long), cudaMemcpyDeviceToHost);
+}
+#endif
 
 int burst_internal_fail(int code, const std::string& msg) { return fail(code, msg); }
 
@@ -339,11 +385,14 @@ int burst_lao_bwd(const burst_hop* hop, const void* q, const void* k, const void
   if (hop->k_len == 0) return BURST_OK;
   cudaStream_t st = (cudaStream_t)stream;
   if (hop->dtype == BURST_DTYPE_BF16) {
+    // the staged kernel reduces whole 128-row TL tiles: needs 128-aligned query ranges
+    const int var = (bwd_variant() == 3 && hop->q_begin % 128 != 0) ? 1 : bwd_variant();
     if (hop->head_dim == 128) {
-      if (use_pair_bwd())
-        return launch_bwd2_bf16(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
+      if (var == 2) return launch_bwd2_bf16(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
+      if (var == 3) return launch_bwd3_bf16<128>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
       return launch_bwd_bf16<128>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
     }
+    if (var == 3) return launch_bwd3_bf16<64>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
     return launch_bwd_bf16<64>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
   }
   switch (hop->head_dim) {

@@ -365,8 +365,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const uint4 v = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
           if (half == (int)crank)
             *reinterpret_cast<uint4*>(dsq_local + off) = v;
-          else
+          else {
+#ifndef BURST_EXP_NO_DSMEM   // timing experiment only: drops the dS exchange
             ptx::st_cluster_v4(dsq_remote + off, v);
+#endif
+          }
         }
       }
       ptx::tmem_wait_st();

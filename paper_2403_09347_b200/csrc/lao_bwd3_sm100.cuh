@@ -1,3 +1,9 @@
+// LAO backward on sm_100a, K/V-stationary, dQ drained through SMEM with TMA bulk
+// reductions (cp.reduce.async.bulk) instead of per-thread red.global: the LSU
+// reduction stream was measured to starve the shared-memory MMA operands
+// (exp/trace_bwd.py).  dO is single-buffered (reloaded as soon as dV retires) to
+// free the 32 KB staging buffer.  Otherwise identical to lao_bwd_sm100.cuh.
+//
 // LAO backward on sm_100a, K/V-stationary.
 //
 // Reference semantics: one call = ring.backward_step (ring.py:221-242) for every
@@ -23,7 +29,7 @@
 #include "ptx.cuh"
 
 namespace burst {
-namespace bwd {
+namespace bwd3 {
 
 constexpr int BM = 128;  // query rows per iteration
 constexpr int BN = 128;  // key rows per CTA
@@ -36,7 +42,9 @@ struct Cfg {
   static constexpr int kTileBytes = kBoxBytes * kBoxes;    // K, V, Q_i, dO_i tiles
   static constexpr int kDsBytes = BN * BM * 2;              // dS^T tile (bf16)
   static constexpr int kStatBytes = 2 * BM * 4;             // lse2_i, D_i
-  static constexpr int kPayload = 2 * kTileBytes + 2 * 2 * kTileBytes + kDsBytes + 2 * kStatBytes;
+  static constexpr int kStageBytes = BM * 64 * 4;            // dQ staging: 64 columns
+  static constexpr int kPayload = 2 * kTileBytes + 2 * kTileBytes + kTileBytes + kDsBytes +
+                                  kStageBytes + 2 * kStatBytes;
   static constexpr int kBarBytes = 128;
   static constexpr int kMaxSmem = 232448;
   static constexpr int kSmemBytes =
@@ -53,7 +61,6 @@ struct Params {
   burst_hop hop;
   float scale_log2, scale;
   int accumulate;
-  long long* trace;   // BURST_TRACE builds only: per-iteration clock64 timeline
 };
 
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -64,19 +71,9 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
-#ifdef BURST_TRACE
-#define BTRACE(ev, i)                                                                        \
-  do {                                                                                       \
-    if (p.trace && (blockIdx.x == 0 || blockIdx.x == 77) && blockIdx.y == 0 && blockIdx.z == 0 && \
-        (i) < 64)                                                                            \
-      p.trace[((blockIdx.x ? 16 : 0) + (ev)) * 64 + (i)] = clock64();                        \
-  } while (0)
-#else
-#define BTRACE(ev, i)
-#endif
 
 template <int D>
-__global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(kThreads, 1) lao_bwd3_kernel(const __grid_constant__ Params p) {
   using C = Cfg<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem;
@@ -89,9 +86,10 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_const
   uint8_t* sK = smem;
   uint8_t* sV = sK + C::kTileBytes;
   uint8_t* sQ = sV + C::kTileBytes;            // [2] stages
-  uint8_t* sdO = sQ + 2 * C::kTileBytes;       // [2] stages
-  uint8_t* sdS = sdO + 2 * C::kTileBytes;
-  float* sStat = reinterpret_cast<float*>(sdS + C::kDsBytes);   // [2][2][BM]
+  uint8_t* sdO = sQ + 2 * C::kTileBytes;       // single buffer
+  uint8_t* sdS = sdO + C::kTileBytes;
+  float* sStage = reinterpret_cast<float*>(sdS + C::kDsBytes);  // dQ staging [16][128] float4
+  float* sStat = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(sStage) + C::kStageBytes);
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sStat) + 2 * C::kStatBytes);
   uint64_t* kv_full = bars;
   uint64_t* qdo_full = bars + 1;   // [2]
@@ -104,7 +102,9 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_const
   uint64_t* dq_empty = bars + 10;
   uint64_t* dkv_full = bars + 11;
   uint64_t* dp_full = bars + 12;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 13);
+  uint64_t* do_full = bars + 13;
+  uint64_t* do_empty = bars + 14;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 15);
 
   const burst_hop& hp = p.hop;
   const int warp = threadIdx.x >> 5;
@@ -145,6 +145,8 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_const
       ptx::mbar_init(dq_empty, BM);
       ptx::mbar_init(dkv_full, 1);
       ptx::mbar_init(dp_full, 1);
+      ptx::mbar_init(do_full, 1);
+      ptx::mbar_init(do_empty, 1);
       ptx::fence_mbar_init();
       ptx::tma_prefetch_desc(&p.tm_q);
       ptx::tma_prefetch_desc(&p.tm_k);
@@ -169,21 +171,32 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_const
         ptx::tma_load_4d(sK + x * C::kBoxBytes, &p.tm_k, kv_full, x * 64, h, (int)k0, b);
         ptx::tma_load_4d(sV + x * C::kBoxBytes, &p.tm_v, kv_full, x * 64, h, (int)k0, b);
       }
-      for (int i = 0; i < nq; ++i) {
-        const int s = i & 1;
-        const int64_t q0 = qtile(i);
-        ptx::mbar_wait(qdo_empty + s, ((i >> 1) & 1) ^ 1); BTRACE(10, i);
-        ptx::mbar_expect_tx(qdo_full + s, 2 * C::kTileBytes + C::kStatBytes);
-        for (int x = 0; x < C::kBoxes; ++x) {
+      // Q_i (+ lse/D stats) double-buffered; dO_i single-buffered, refilled when dV retires
+      auto load_q = [&](int j) {
+        const int s = j & 1;
+        const int64_t q0 = qtile(j);
+        ptx::mbar_wait(qdo_empty + s, ((j >> 1) & 1) ^ 1);
+        ptx::mbar_expect_tx(qdo_full + s, C::kTileBytes + C::kStatBytes);
+        for (int x = 0; x < C::kBoxes; ++x)
           ptx::tma_load_4d(sQ + s * C::kTileBytes + x * C::kBoxBytes, &p.tm_q, qdo_full + s,
                            x * 64, h, (int)q0, b);
-          ptx::tma_load_4d(sdO + s * C::kTileBytes + x * C::kBoxBytes, &p.tm_do, qdo_full + s,
-                           x * 64, h, (int)q0, b);
-        }
         const float* st = p.stats + bh * NTq * 128 + q0;
         bulk_load(sStat + s * 2 * BM, st, BM * 4, qdo_full + s);
         bulk_load(sStat + s * 2 * BM + BM, st + (int64_t)hp.batch * hp.heads * NTq * 128, BM * 4,
                   qdo_full + s);
+      };
+      auto load_do = [&](int j) {
+        ptx::mbar_wait(do_empty, (j & 1) ^ 1);
+        ptx::mbar_expect_tx(do_full, C::kTileBytes);
+        for (int x = 0; x < C::kBoxes; ++x)
+          ptx::tma_load_4d(sdO + x * C::kBoxBytes, &p.tm_do, do_full, x * 64, h, (int)qtile(j), b);
+      };
+      load_q(0);
+      load_do(0);
+      if (nq > 1) load_q(1);
+      for (int i = 0; i < nq; ++i) {      // release order: dO after dV_i, Q stage after dK_i
+        if (i + 1 < nq) load_do(i + 1);
+        if (i + 2 < nq) load_q(i + 2);
       }
     }
   } else if (warp == 9) {
@@ -205,8 +218,8 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_const
                       ptx::make_sdesc(q + off, 0, 1024), id_kk, kk > 0);
         }
       };
-      auto dpt_mma = [&](int stage) {  // dP^T = V dO^T
-        const uint32_t dO = adO + stage * C::kTileBytes;
+      auto dpt_mma = [&](int) {  // dP^T = V dO^T
+        const uint32_t dO = adO;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * C::kBoxBytes + (kk & 3) * 32;
@@ -219,28 +232,31 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_const
       ptx::tc_fence_after();
       st_mma(0);
       ptx::mma_commit(s_full);
+      ptx::mbar_wait(do_full, 0);
+      ptx::tc_fence_after();
       dpt_mma(0);
       ptx::mma_commit(dp_full);
       for (int i = 0; i < nq; ++i) {
         const int s = i & 1;
         const bool more = i + 1 < nq;
-        const uint32_t q = aQ + s * C::kTileBytes, dO = adO + s * C::kTileBytes;
+        const uint32_t q = aQ + s * C::kTileBytes, dO = adO;
         // dV += P^T dO   (A = P^T from TMEM, B = dO MN-major, reduction over queries)
-        ptx::mbar_wait(p_full, i & 1); BTRACE(0, i);
+        ptx::mbar_wait(p_full, i & 1);
         ptx::tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < BM / 16; ++kk)
           ptx::mma_ts(tbase + kDV, tbase + kS + kk * 8,
                       ptx::make_sdesc(dO + kk * 2048, C::kBoxBytes, 1024), id_kmn,
                       (i > 0 || kk > 0) ? 1u : 0u);
+        ptx::mma_commit(do_empty);
         if (more) {
-          ptx::mbar_wait(qdo_full + (s ^ 1), ((i + 1) >> 1) & 1); BTRACE(11, i);
+          ptx::mbar_wait(qdo_full + (s ^ 1), ((i + 1) >> 1) & 1);
           ptx::tc_fence_after();
           st_mma(s ^ 1);
           ptx::mma_commit(s_full);
         }
         // dK += dS^T Q ; dQ_i = dS K  (into the dP^T columns, already consumed)
-        ptx::mbar_wait(ds_full, i & 1); BTRACE(1, i);
+        ptx::mbar_wait(ds_full, i & 1);
         ptx::tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < BM / 16; ++kk) {
@@ -257,7 +273,8 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_const
         ptx::mma_commit(ds_empty);
         ptx::mma_commit(qdo_empty + s);
         if (more) {
-          ptx::mbar_wait(dq_empty, i & 1); BTRACE(2, i);
+          ptx::mbar_wait(dq_empty, i & 1);
+          ptx::mbar_wait(do_full, (i + 1) & 1);
           ptx::tc_fence_after();
           dpt_mma(s ^ 1);
           ptx::mma_commit(dp_full);
@@ -285,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_const
       const int hi = !kvalid ? 0 : (hi64 > BM ? BM : (hi64 < 0 ? 0 : (int)hi64));
       const bool warp_full = __all_sync(0xffffffffu, lo == 0 && hi == BM);
       ptx::mbar_wait(qdo_full + s, (i >> 1) & 1);
-      ptx::mbar_wait(s_full, i & 1); BTRACE(3, i);
+      ptx::mbar_wait(s_full, i & 1);
       ptx::tc_fence_after();
       const float4* lse4 = reinterpret_cast<const float4*>(sStat + s * 2 * BM);
       const float4* dst4 = lse4 + BM / 4;
@@ -320,9 +337,9 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_const
       }
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(p_full); BTRACE(4, i);
+      ptx::mbar_arrive(p_full);
 
-      ptx::mbar_wait(dp_full, i & 1); BTRACE(5, i);
+      ptx::mbar_wait(dp_full, i & 1);
       ptx::mbar_wait(ds_empty, (i & 1) ^ 1);
       ptx::tc_fence_after();
 #pragma unroll
@@ -351,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_const
       }
       ptx::fence_proxy_async_smem();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(ds_full); BTRACE(6, i);
+      ptx::mbar_arrive(ds_full);
     }
     // -------------------------------------------------------- dK / dV epilogue
     if (nq > 0) {
@@ -390,30 +407,46 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_const
     }
   } else if (warp < 8) {
     // ------------------------------------------------------------ dQ drain warpgroup
+    // TMEM -> registers -> SMEM staging (64 columns at a time) -> one TMA bulk reduction
+    // per half tile into the TL workspace (each 64-column half of a 128-row tile is a
+    // contiguous 32 KB run there).
     const int t = threadIdx.x & 127;           // query row within the tile
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    float4* stg = reinterpret_cast<float4*>(sStage);
     for (int i = 0; i < nq; ++i) {
-      const int64_t qrow = qtile(i) + t;
-      const bool qvalid = qrow < q_end && qrow < hp.n_q;
-      ptx::mbar_wait(dq_full, i & 1); BTRACE(7, i);
+      const int64_t q0 = qtile(i);
+      const bool qvalid = q0 + t < q_end && q0 + t < hp.n_q;
+      ptx::mbar_wait(dq_full, i & 1);
       ptx::tc_fence_after();
-      uint32_t r[D];
+#pragma unroll 1
+      for (int half = 0; half < D / 64; ++half) {
+        uint32_t r[64];
+        ptx::tmem_ld32(tbase + lane_off + kDP + half * 64, *reinterpret_cast<uint32_t(*)[32]>(r));
+        ptx::tmem_ld32(tbase + lane_off + kDP + half * 64 + 32,
+                       *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+        ptx::tmem_wait_ld();
+        ptx::reg_fence(r);
+        if (half == D / 64 - 1) {
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(dq_empty);
+        }
+        if (t == 0) ptx::bulk_wait_read_all();   // staging consumed by the previous reduction
+        ptx::named_bar_sync(1, 128);
+        const float sc = qvalid ? p.scale : 0.f;
 #pragma unroll
-      for (int cc = 0; cc < D / 32; ++cc)
-        ptx::tmem_ld32(tbase + lane_off + kDP + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(r + cc * 32));
-      ptx::tmem_wait_ld();
-      ptx::reg_fence(r);
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(dq_empty); BTRACE(8, i);
-      if (qvalid) {
-        float* base = p.dq_acc + tl_index(bh, qrow, 0, D, NTq);
-#pragma unroll
-        for (int j = 0; j < D; j += 4)   // next 4-column group: 128 rows x 4 floats further
-          ptx::red_add_v4(base + (size_t)(j >> 2) * 512, __uint_as_float(r[j]) * p.scale,
-                          __uint_as_float(r[j + 1]) * p.scale, __uint_as_float(r[j + 2]) * p.scale,
-                          __uint_as_float(r[j + 3]) * p.scale);
+        for (int g = 0; g < 16; ++g)
+          stg[g * 128 + t] = make_float4(__uint_as_float(r[4 * g]) * sc, __uint_as_float(r[4 * g + 1]) * sc,
+                                         __uint_as_float(r[4 * g + 2]) * sc, __uint_as_float(r[4 * g + 3]) * sc);
+        ptx::fence_proxy_async_smem();
+        ptx::named_bar_sync(1, 128);
+        if (t == 0) {
+          ptx::bulk_reduce_add_f32(p.dq_acc + tl_index(bh, q0, half * 64, D, NTq), sStage,
+                                   C::kStageBytes);
+          ptx::bulk_commit();
+        }
       }
     }
+    if (t == 0) ptx::bulk_wait_all();
   }
 
   __syncwarp();
@@ -425,5 +458,5 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_const
   }
 }
 
-}  // namespace bwd
+}  // namespace bwd3
 }  // namespace burst
