@@ -61,6 +61,7 @@ struct Params {
   burst_hop hop;
   float scale_log2, scale;
   int accumulate;
+  long long* trace;   // BURST_TRACE builds only: per-iteration clock64 timeline
 };
 
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -71,6 +72,17 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
+
+#ifdef BURST_TRACE
+#define BTRACE(ev, i)                                                                        \
+  do {                                                                                       \
+    if (p.trace && (blockIdx.x == 0 || blockIdx.x == 77) && blockIdx.y == 0 && blockIdx.z == 0 && \
+        (i) < 64)                                                                            \
+      p.trace[((blockIdx.x ? 16 : 0) + (ev)) * 64 + (i)] = clock64();                        \
+  } while (0)
+#else
+#define BTRACE(ev, i)
+#endif
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1) lao_bwd3_kernel(const __grid_constant__ Params p) {
@@ -241,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd3_kernel(const __grid_cons
         const bool more = i + 1 < nq;
         const uint32_t q = aQ + s * C::kTileBytes, dO = adO;
         // dV += P^T dO   (A = P^T from TMEM, B = dO MN-major, reduction over queries)
-        ptx::mbar_wait(p_full, i & 1);
+        ptx::mbar_wait(p_full, i & 1); BTRACE(0, i);
         ptx::tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < BM / 16; ++kk)
@@ -250,13 +262,13 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd3_kernel(const __grid_cons
                       (i > 0 || kk > 0) ? 1u : 0u);
         ptx::mma_commit(do_empty);
         if (more) {
-          ptx::mbar_wait(qdo_full + (s ^ 1), ((i + 1) >> 1) & 1);
+          ptx::mbar_wait(qdo_full + (s ^ 1), ((i + 1) >> 1) & 1); BTRACE(11, i);
           ptx::tc_fence_after();
           st_mma(s ^ 1);
           ptx::mma_commit(s_full);
         }
         // dK += dS^T Q ; dQ_i = dS K  (into the dP^T columns, already consumed)
-        ptx::mbar_wait(ds_full, i & 1);
+        ptx::mbar_wait(ds_full, i & 1); BTRACE(1, i);
         ptx::tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < BM / 16; ++kk) {
@@ -273,8 +285,8 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd3_kernel(const __grid_cons
         ptx::mma_commit(ds_empty);
         ptx::mma_commit(qdo_empty + s);
         if (more) {
-          ptx::mbar_wait(dq_empty, i & 1);
-          ptx::mbar_wait(do_full, (i + 1) & 1);
+          ptx::mbar_wait(dq_empty, i & 1); BTRACE(2, i);
+          ptx::mbar_wait(do_full, (i + 1) & 1); BTRACE(10, i);
           ptx::tc_fence_after();
           dpt_mma(s ^ 1);
           ptx::mma_commit(dp_full);
@@ -302,7 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd3_kernel(const __grid_cons
       const int hi = !kvalid ? 0 : (hi64 > BM ? BM : (hi64 < 0 ? 0 : (int)hi64));
       const bool warp_full = __all_sync(0xffffffffu, lo == 0 && hi == BM);
       ptx::mbar_wait(qdo_full + s, (i >> 1) & 1);
-      ptx::mbar_wait(s_full, i & 1);
+      ptx::mbar_wait(s_full, i & 1); BTRACE(3, i);
       ptx::tc_fence_after();
       const float4* lse4 = reinterpret_cast<const float4*>(sStat + s * 2 * BM);
       const float4* dst4 = lse4 + BM / 4;
@@ -337,9 +349,9 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd3_kernel(const __grid_cons
       }
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(p_full);
+      ptx::mbar_arrive(p_full); BTRACE(4, i);
 
-      ptx::mbar_wait(dp_full, i & 1);
+      ptx::mbar_wait(dp_full, i & 1); BTRACE(5, i);
       ptx::mbar_wait(ds_empty, (i & 1) ^ 1);
       ptx::tc_fence_after();
 #pragma unroll
@@ -368,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd3_kernel(const __grid_cons
       }
       ptx::fence_proxy_async_smem();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(ds_full);
+      ptx::mbar_arrive(ds_full); BTRACE(6, i);
     }
     // -------------------------------------------------------- dK / dV epilogue
     if (nq > 0) {
@@ -416,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd3_kernel(const __grid_cons
     for (int i = 0; i < nq; ++i) {
       const int64_t q0 = qtile(i);
       const bool qvalid = q0 + t < q_end && q0 + t < hp.n_q;
-      ptx::mbar_wait(dq_full, i & 1);
+      ptx::mbar_wait(dq_full, i & 1); BTRACE(7, i);
       ptx::tc_fence_after();
 #pragma unroll 1
       for (int half = 0; half < D / 64; ++half) {
@@ -428,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd3_kernel(const __grid_cons
         ptx::reg_fence(r);
         if (half == D / 64 - 1) {
           ptx::tc_fence_before();
-          ptx::mbar_arrive(dq_empty);
+          ptx::mbar_arrive(dq_empty); BTRACE(8, i);
         }
         if (t == 0) ptx::bulk_wait_read_all();   // staging consumed by the previous reduction
         ptx::named_bar_sync(1, 128);
@@ -442,7 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd3_kernel(const __grid_cons
         if (t == 0) {
           ptx::bulk_reduce_add_f32(p.dq_acc + tl_index(bh, q0, half * 64, D, NTq), sStage,
                                    C::kStageBytes);
-          ptx::bulk_commit();
+          ptx::bulk_commit(); BTRACE(9, i);
         }
       }
     }
