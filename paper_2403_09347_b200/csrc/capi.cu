@@ -216,6 +216,9 @@ int launch_bwd2_bf16(const burst_hop* h, const void* q, const void* k, const voi
   p.scale_log2 = h->softmax_scale * kLog2e;
   p.scale = h->softmax_scale;
   p.accumulate = acc;
+#ifdef BURST_TRACE
+  p.trace = trace_buffer();
+#endif
   static std::once_flag once;
   static int attr_rc = 0;
   std::call_once(once, [] { attr_rc = set_smem(bwd2::lao_bwd2_kernel, bwd2::kSmemBytes); });

@@ -46,12 +46,14 @@ struct Params {
   burst_hop hop;
   float scale_log2, scale;
   int accumulate;
+  long long* trace;   // BURST_TRACE builds only
 };
 
 namespace L {   // shared-memory layout (bytes from the 1024-aligned base)
 constexpr int K = 0, V = 32768, KQ = 65536, DSQ = 98304;
 constexpr int QA = 131072, QB = 147456, DOA = 163840, DOB = 180224;
-constexpr int STATS = 196608;                    // kStatSlots x (lse2[128], D[128])
+constexpr int XS = 196608;                       // outgoing dS half for the peer (16 KB)
+constexpr int STATS = 212992;                    // kStatSlots x (lse2[128], D[128])
 constexpr int BARS = STATS + kStatSlots * 1024;  // barriers
 constexpr int kBytes = BARS + 64 * 8;
 }  // namespace L
@@ -61,7 +63,7 @@ constexpr int kSmemBytes = L::kBytes + 1024;
 enum {
   B_KV = 0, B_QA_F, B_QA_E, B_QB_F, B_QB_E, B_DA_F, B_DA_E, B_DB_F, B_DB_E,
   B_ST_F, B_ST_E = B_ST_F + kStatSlots,
-  B_S = B_ST_E + kStatSlots, B_DP, B_P, B_DS, B_DQF, B_DQE, B_DSQE, B_DKV, B_COUNT
+  B_S = B_ST_E + kStatSlots, B_DP, B_P, B_DS, B_DQF, B_DQE, B_DSQE, B_DKV, B_X, B_XR, B_COUNT
 };
 
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -71,6 +73,16 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(ptx::smem_u32(bar))
       : "memory");
 }
+
+#ifdef BURST_TRACE
+#define BTRACE2(ev, i)                                                                       \
+  do {                                                                                       \
+    if (p.trace && blockIdx.x < 2 && blockIdx.y == 0 && blockIdx.z == 0 && (i) < 64)         \
+      p.trace[(blockIdx.x * 16 + (ev)) * 64 + (i)] = clock64();                              \
+  } while (0)
+#else
+#define BTRACE2(ev, i)
+#endif
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     lao_bwd2_kernel(const __grid_constant__ Params p) {
@@ -231,8 +243,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int i = 0; i < nq; ++i) {
         const bool more = i + 1 < nq;
         // dV += P^T dO
-        ptx::mbar_wait_cluster(bar + B_P, i & 1);
-        ptx::mbar_wait(bar + B_DB_F, i & 1);
+        ptx::mbar_wait(bar + B_P, i & 1); BTRACE2(0, i);
+        ptx::mbar_wait(bar + B_DB_F, i & 1); BTRACE2(9, i);
         ptx::tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < BM / 16; ++kk)
@@ -241,14 +253,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                        (i > 0 || kk > 0) ? 1u : 0u);
         ptx::mma2_commit(bar + B_DB_E);
         if (more) {   // S^T_{i+1} overlaps the dS_i phase
-          ptx::mbar_wait(bar + B_QA_F, (i + 1) & 1);
+          ptx::mbar_wait(bar + B_QA_F, (i + 1) & 1); BTRACE2(11, i);
           ptx::tc_fence_after();
           st_mma();
           ptx::mma2_commit(bar + B_S);
           ptx::mma2_commit(bar + B_QA_E);
         }
         // dK += dS^T Q ; dQ = dS K
-        ptx::mbar_wait_cluster(bar + B_DS, i & 1);
+        ptx::mbar_wait(bar + B_DS, i & 1); BTRACE2(1, i);
         ptx::mbar_wait(bar + B_QB_F, i & 1);
         ptx::tc_fence_after();
 #pragma unroll
@@ -257,6 +269,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                        ptx::make_sdesc(a0 + L::QB + kk * 2048, 0, 1024), id_kd,
                        (i > 0 || kk > 0) ? 1u : 0u);
         ptx::mma2_commit(bar + B_QB_E);
+        ptx::mbar_wait(bar + B_X, i & 1);     // peer's dS half landed here
+        ptx::mbar_wait(bar + B_XR, i & 1);    // ... and ours landed in the peer (relayed)
+        ptx::tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < (2 * BN) / 16; ++kk)
           ptx::mma2_ss(tbase + kDQ, ptx::make_sdesc(a0 + L::DSQ + kk * 2048, 0, 1024),
@@ -264,8 +279,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         ptx::mma2_commit(bar + B_DQF);
         ptx::mma2_commit(bar + B_DSQE);
         if (more) {
-          ptx::mbar_wait_cluster(bar + B_DQE, i & 1);
-          ptx::mbar_wait(bar + B_DA_F, (i + 1) & 1);
+          ptx::mbar_wait(bar + B_DQE, i & 1); BTRACE2(2, i);
+          ptx::mbar_wait(bar + B_DA_F, (i + 1) & 1); BTRACE2(10, i);
           ptx::tc_fence_after();
           dpt_mma();
           ptx::mma2_commit(bar + B_DP);
@@ -273,6 +288,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
       }
       ptx::mma2_commit(bar + B_DKV);
+    } else if (warp == 10 && lane == 0 && !leader && nq > 0) {
+      // relay: tell the leader that the leader's dS half has landed in this CTA
+      const uint32_t xr = ptx::leader_addr(bar + B_XR);
+      for (int i = 0; i < nq; ++i) {
+        ptx::mbar_wait(bar + B_X, i & 1);
+        ptx::mbar_arrive_remote(xr);
+      }
     }
   } else if (warp < 4) {
     // ------------------------------------------------------------ P / dS warpgroup
@@ -285,10 +307,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int64_t qfirst = hp.causal ? count_le(hp.q_map, hp.n_q, kpos - 1) : 0;
     const float c2 = p.scale_log2;
     const uint32_t p_bar = ptx::leader_addr(bar + B_P), ds_bar = ptx::leader_addr(bar + B_DS);
+    const uint32_t xs_peer = ptx::peer_addr(sm + L::DSQ + crank * 16384, crank ^ 1u);
+    const uint32_t xbar_peer = ptx::peer_addr(bar + B_X, crank ^ 1u);
+    uint8_t* xs_row = sm + L::XS + t * 128;
     // this key row inside both CTAs' dS_dQ buffers: row 128*crank + t (K-dim = pair's keys)
     const uint32_t dsq_row = (uint32_t)(crank * BN + t);
     uint8_t* dsq_local = sm + L::DSQ + (dsq_row >> 7) * 16384 + (dsq_row & 127) * 128;
-    const uint32_t dsq_remote = ptx::peer_addr(dsq_local, crank ^ 1u);
     for (int i = 0; i < nq; ++i) {
       const int s = i % kStatSlots;
       const int64_t q0 = qtile(i);
@@ -297,7 +321,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int hi = !kvalid ? 0 : (hi64 > BM ? BM : (hi64 < 0 ? 0 : (int)hi64));
       const bool warp_full = __all_sync(0xffffffffu, lo == 0 && hi == BM);
       ptx::mbar_wait(bar + B_ST_F + s, (i / kStatSlots) & 1);
-      ptx::mbar_wait(bar + B_S, i & 1);
+      ptx::mbar_wait(bar + B_S, i & 1); BTRACE2(3, i);
       ptx::tc_fence_after();
       const float4* lse4 = reinterpret_cast<const float4*>(sStat + s * 256);
       const float4* dst4 = lse4 + BM / 4;
@@ -332,12 +356,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
-      ptx::mbar_arrive_cluster(p_bar);
+      ptx::mbar_arrive_to(p_bar, leader, bar + B_P); BTRACE2(4, i);
 
       // dS = P (dP - D); chunks of 32 queries from the top so every dS^T column
       // written into [192,256) has already been read as dP^T
-      ptx::mbar_wait(bar + B_DP, i & 1);
+      ptx::mbar_wait(bar + B_DP, i & 1); BTRACE2(5, i);
       ptx::mbar_wait(bar + B_DSQE, (i & 1) ^ 1);
+      if (t == 0) ptx::mbar_expect_tx(bar + B_X, 16384);   // the peer's half of this tile
       ptx::tc_fence_after();
 #pragma unroll
       for (int cc = 3; cc >= 0; --cc) {
@@ -363,20 +388,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const int ch = (cc & 1) * 4 + u;
           const uint32_t off = (uint32_t)((ch ^ (dsq_row & 7)) << 4);
           const uint4 v = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
-          if (half == (int)crank)
-            *reinterpret_cast<uint4*>(dsq_local + off) = v;
-          else {
-#ifndef BURST_EXP_NO_DSMEM   // timing experiment only: drops the dS exchange
-            ptx::st_cluster_v4(dsq_remote + off, v);
-#endif
-          }
+          *reinterpret_cast<uint4*>((half == (int)crank ? dsq_local : xs_row) + off) = v;
         }
       }
       ptx::tmem_wait_st();
       ptx::fence_proxy_async_smem();
-      ptx::fence_proxy_async_cluster();
+      ptx::named_bar_sync(2, BN);
+      if (t == 0)   // one TMA bulk copy ships the peer's half: SMEM -> peer SMEM, tx on its B_X
+        ptx::bulk_copy_to_peer(xs_peer, sm + L::XS, 16384, xbar_peer);
       ptx::tc_fence_before();
-      ptx::mbar_arrive_cluster(ds_bar);
+      ptx::mbar_arrive_to(ds_bar, leader, bar + B_DS); BTRACE2(6, i);
       ptx::mbar_arrive(bar + B_ST_E + s);
     }
     // -------------------------------------------------------- dK / dV epilogue
@@ -424,7 +445,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int i = 0; i < nq; ++i) {
       const int64_t qrow = qtile(i) + crank * 64 + (L & 63);
       const bool qvalid = qrow < q_end && qrow < hp.n_q;
-      ptx::mbar_wait(bar + B_DQF, i & 1);
+      ptx::mbar_wait(bar + B_DQF, i & 1); BTRACE2(7, i);
       ptx::tc_fence_after();
       uint32_t r[64];
       ptx::tmem_ld32(tbase + lane_off + kDQ, *reinterpret_cast<uint32_t(*)[32]>(r));
@@ -432,7 +453,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       ptx::tmem_wait_ld();
       ptx::reg_fence(r);
       ptx::tc_fence_before();
-      ptx::mbar_arrive_cluster(dqe_bar);
+      ptx::mbar_arrive_to(dqe_bar, leader, bar + B_DQE); BTRACE2(8, i);
       if (qvalid) {
         float* base = p.dq_acc + tl_index(bh, qrow, dbase, D, NTq);
 #pragma unroll

@@ -430,25 +430,26 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd3_kernel(const __grid_cons
       const bool qvalid = q0 + t < q_end && q0 + t < hp.n_q;
       ptx::mbar_wait(dq_full, i & 1); BTRACE(7, i);
       ptx::tc_fence_after();
-#pragma unroll 1
+      // whole tile to registers first: TMEM is released before any staging work
+      uint32_t r[D];
+#pragma unroll
+      for (int cc = 0; cc < D / 32; ++cc)
+        ptx::tmem_ld32(tbase + lane_off + kDP + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(r + cc * 32));
+      ptx::tmem_wait_ld();
+      ptx::reg_fence(r);
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(dq_empty); BTRACE(8, i);
+      const float sc = qvalid ? p.scale : 0.f;
+#pragma unroll
       for (int half = 0; half < D / 64; ++half) {
-        uint32_t r[64];
-        ptx::tmem_ld32(tbase + lane_off + kDP + half * 64, *reinterpret_cast<uint32_t(*)[32]>(r));
-        ptx::tmem_ld32(tbase + lane_off + kDP + half * 64 + 32,
-                       *reinterpret_cast<uint32_t(*)[32]>(r + 32));
-        ptx::tmem_wait_ld();
-        ptx::reg_fence(r);
-        if (half == D / 64 - 1) {
-          ptx::tc_fence_before();
-          ptx::mbar_arrive(dq_empty); BTRACE(8, i);
-        }
         if (t == 0) ptx::bulk_wait_read_all();   // staging consumed by the previous reduction
         ptx::named_bar_sync(1, 128);
-        const float sc = qvalid ? p.scale : 0.f;
 #pragma unroll
-        for (int g = 0; g < 16; ++g)
-          stg[g * 128 + t] = make_float4(__uint_as_float(r[4 * g]) * sc, __uint_as_float(r[4 * g + 1]) * sc,
-                                         __uint_as_float(r[4 * g + 2]) * sc, __uint_as_float(r[4 * g + 3]) * sc);
+        for (int g = 0; g < 16; ++g) {
+          const int c = half * 64 + 4 * g;
+          stg[g * 128 + t] = make_float4(__uint_as_float(r[c]) * sc, __uint_as_float(r[c + 1]) * sc,
+                                         __uint_as_float(r[c + 2]) * sc, __uint_as_float(r[c + 3]) * sc);
+        }
         ptx::fence_proxy_async_smem();
         ptx::named_bar_sync(1, 128);
         if (t == 0) {

@@ -228,6 +228,29 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
 }
+// arrive with default (release.cta) semantics on a barrier given by its shared::cluster
+// address; cheap, used for tcgen05-ordered handoffs inside a CTA pair
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// local arrive in the leader, remote arrive from the peer
+__device__ __forceinline__ void mbar_arrive_to(uint32_t leader_cluster_addr, bool is_leader,
+                                               uint64_t* local_bar) {
+  if (is_leader)
+    mbar_arrive(local_bar);
+  else
+    mbar_arrive_remote(leader_cluster_addr);
+}
+// TMA bulk copy of `bytes` from this CTA's SMEM into the peer CTA's SMEM; completes tx
+// bytes on the peer's mbarrier
+__device__ __forceinline__ void bulk_copy_to_peer(uint32_t peer_dst, const void* src, uint32_t bytes,
+                                                  uint32_t peer_bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          peer_dst),
+      "r"(smem_u32(src)), "r"(bytes), "r"(peer_bar)
+      : "memory");
+}
 __device__ __forceinline__ void st_cluster_v4(uint32_t cluster_addr, uint4 v) {
   asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(cluster_addr), "r"(v.x),
                "r"(v.y), "r"(v.z), "r"(v.w)
