@@ -48,30 +48,34 @@ def _transport_for(group):
 
 class _BurstAttnFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, q, k, v, scale, causal, zigzag, transport, kernels):
-        o, lse = ring_forward(q, k, v, scale, causal, zigzag, transport, kernels)
+    def forward(ctx, q, k, v, scale, causal, zigzag, transport, kernels, n_valid):
+        o, lse = ring_forward(q, k, v, scale, causal, zigzag, transport, kernels, n_valid)
         ctx.save_for_backward(q, k, v, o, lse)
-        ctx.cfg = (scale, causal, zigzag, transport, kernels)
+        ctx.cfg = (scale, causal, zigzag, transport, kernels, n_valid)
         ctx.mark_non_differentiable(lse)
         return o, lse
 
     @staticmethod
     def backward(ctx, do, _dlse):
         q, k, v, o, lse = ctx.saved_tensors
-        scale, causal, zigzag, transport, kernels = ctx.cfg
+        scale, causal, zigzag, transport, kernels, n_valid = ctx.cfg
         dq, dk, dv = ring_backward(q, k, v, o, lse, do.contiguous(), scale, causal, zigzag,
-                                   transport, kernels)
-        return dq, dk, dv, None, None, None, None, None
+                                   transport, kernels, n_valid)
+        return dq, dk, dv, None, None, None, None, None, None
 
 
 def burst_attn_func(q, k, v, causal: bool = False, softmax_scale: float | None = None,
-                    group=None, zigzag: bool | None = None, *, _transport=None, _kernels=None):
+                    group=None, zigzag: bool | None = None, valid_len: int | None = None, *,
+                    _transport=None, _kernels=None):
     """BurstAttention over the ranks of `group` (NCCL ring over NVLink).
 
     q, k, v: [batch, n_local, heads, head_dim] shards of the global sequence
     (contiguous blocks, or zigzag chunks {rank, 2G-1-rank} when causal and
     zigzag -- the default for causal with G > 1; see `schedule.shard`).
     Returns (out [batch, n_local, heads, head_dim], lse [batch, heads, n_local]).
+    `valid_len`: real global sequence length when the shards were zero-padded to
+    a multiple of G (2G for zigzag); padded keys are excluded, padded rows of the
+    outputs are meaningless (the reference's pad=True, ring.py:111-115).
     """
     check_qkv(q, k, v) if _kernels is None else None
     if q.shape[1] != k.shape[1]:
@@ -85,7 +89,10 @@ def burst_attn_func(q, k, v, causal: bool = False, softmax_scale: float | None =
         zigzag = bool(causal) and transport.world > 1
     if zigzag and q.shape[1] % 2:
         raise ShapeError("zigzag shards need an even local length")
-    return _BurstAttnFn.apply(q, k, v, scale, bool(causal), bool(zigzag), transport, kernels)
+    if valid_len is not None and not 0 < valid_len <= q.shape[1] * transport.world:
+        raise ShapeError(f"valid_len={valid_len} outside (0, {q.shape[1] * transport.world}]")
+    return _BurstAttnFn.apply(q, k, v, scale, bool(causal), bool(zigzag), transport, kernels,
+                              valid_len)
 
 
 @dataclass
@@ -99,7 +106,8 @@ class PassResult:
 
 
 def run_ring_pass(q, k, v, world: int, causal: bool = False, softmax_scale: float | None = None,
-                  dout=None, zigzag: bool | None = None, kernels=None) -> PassResult:
+                  dout=None, zigzag: bool | None = None, kernels=None,
+                  pad: bool = False) -> PassResult:
     """Whole-ring forward (+ backward when `dout` is given) of GLOBAL tensors
     [batch, N, heads, head_dim] over `world` simulated devices on this GPU.
 
@@ -115,27 +123,42 @@ def run_ring_pass(q, k, v, world: int, causal: bool = False, softmax_scale: floa
     if zigzag is None:
         zigzag = bool(causal) and world > 1
     N = q.shape[1]
-    if N % (2 * world if zigzag else world):
-        raise ConfigError(f"gpus={world} does not divide seq={N}" + (" into 2G chunks" if zigzag else ""))
+    # zigzag hop classes start at chunk boundaries; the bf16 kernels need them 8-aligned
+    unit = 2 * world * (8 if q.dtype == torch.bfloat16 else 1) if zigzag else world
+    n_valid = None
+    if N % unit:
+        if not pad:
+            raise ConfigError(f"gpus={world} does not divide seq={N}"
+                              + (" into 2G chunks" if zigzag else "")
+                              + "; enable pad to zero-fill the remainder")
+        # RunConfig.pad / ring.partition(pad=True) (runner.py:96-98, ring.py:111-115)
+        n_pad = -(-N // unit) * unit
+        if zigzag and n_pad - N >= n_pad // unit:
+            raise ConfigError(f"seq={N} too short to zero-pad into {unit} zigzag chunks")
+        n_valid = N
+        padz = lambda t: torch.cat([t, t.new_zeros(t.shape[0], n_pad - N, *t.shape[2:])], dim=1)
+        q, k, v = padz(q), padz(k), padz(v)
+        dout = padz(dout) if dout is not None else None
     scale = default_scale(q.shape[-1]) if softmax_scale is None else float(softmax_scale)
     shards = [[shard(t, r, world, zigzag) for r in range(world)] for t in (q, k, v)]
     do_sh = [shard(dout, r, world, zigzag) for r in range(world)] if dout is not None else None
 
     def one(rank, transport):
         qs, ks, vs = shards[0][rank], shards[1][rank], shards[2][rank]
-        o, lse = ring_forward(qs, ks, vs, scale, causal, zigzag, transport, kernels)
+        o, lse = ring_forward(qs, ks, vs, scale, causal, zigzag, transport, kernels, n_valid)
         if do_sh is None:
             return o, lse, None
         g = ring_backward(qs, ks, vs, o, lse, do_sh[rank], scale, causal, zigzag, transport,
-                          kernels)
+                          kernels, n_valid)
         return o, lse, g
 
     res = run_ranks(world, one)
-    out = unshard([x[0] for x in res], zigzag, dim=1)
-    lse = unshard([x[1] for x in res], zigzag, dim=2)
+    # _collect drops padded rows (sim.py:450-471)
+    out = unshard([x[0] for x in res], zigzag, dim=1)[:, :N]
+    lse = unshard([x[1] for x in res], zigzag, dim=2)[:, :, :N]
     if dout is None:
         return PassResult(out, lse)
-    dq = unshard([x[2][0] for x in res], zigzag, dim=1)
-    dk = unshard([x[2][1] for x in res], zigzag, dim=1)
-    dv = unshard([x[2][2] for x in res], zigzag, dim=1)
+    dq = unshard([x[2][0] for x in res], zigzag, dim=1)[:, :N]
+    dk = unshard([x[2][1] for x in res], zigzag, dim=1)[:, :N]
+    dv = unshard([x[2][2] for x in res], zigzag, dim=1)[:, :N]
     return PassResult(out, lse, dq, dk, dv)

@@ -239,8 +239,10 @@ class LoopbackTransport:
 # the hop loops
 # ---------------------------------------------------------------------------
 
-def ring_forward(q, k, v, scale: float, causal: bool, zigzag: bool, transport, kernels):
-    """One rank's forward pass.  Returns (O [B,n,H,D], lse [B,H,n] natural log)."""
+def ring_forward(q, k, v, scale: float, causal: bool, zigzag: bool, transport, kernels,
+                 n_valid: int | None = None):
+    """One rank's forward pass.  Returns (O [B,n,H,D], lse [B,H,n] natural log).
+    `n_valid`: real global length when the shards are zero-padded (reference pad=True)."""
     B, n, H, D = q.shape
     G, r = transport.world, transport.rank
     S = _Streams(q.device)
@@ -251,7 +253,7 @@ def ring_forward(q, k, v, scale: float, causal: bool, zigzag: bool, transport, k
     spare = None
     finalized = False
     for h in range(G):
-        plan = plan_hop(r, G, h, n, causal, zigzag)
+        plan = plan_hop(r, G, h, n, causal, zigzag, n_valid)
         exchanged = False
         if h < G - 1:
             if spare is None:
@@ -277,14 +279,14 @@ def ring_forward(q, k, v, scale: float, causal: bool, zigzag: bool, transport, k
 
 
 def _part_exchange(r: int, G: int, n: int, causal: bool, zigzag: bool, hop: int, send_bufs,
-                   kernels, like_k, like_v):
+                   kernels, like_k, like_v, n_valid=None):
     """Ops moving the dK/dV contribution computed at `hop` to its home rank."""
     ops, recv_bufs = [], None
-    mine = plan_hop(r, G, hop, n, causal, zigzag)
+    mine = plan_hop(r, G, hop, n, causal, zigzag, n_valid)
     if not mine.skip:
         ops += [(SEND, send_bufs[0], mine.src), (SEND, send_bufs[1], mine.src)]
     c = contributor_to(r, G, hop)
-    theirs = plan_hop(c, G, hop, n, causal, zigzag)
+    theirs = plan_hop(c, G, hop, n, causal, zigzag, n_valid)
     if not theirs.skip:
         recv_bufs = (kernels.part(like_k), kernels.part(like_v))
         ops += [(RECV, recv_bufs[0], c), (RECV, recv_bufs[1], c)]
@@ -292,7 +294,7 @@ def _part_exchange(r: int, G: int, n: int, causal: bool, zigzag: bool, hop: int,
 
 
 def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: bool, transport,
-                  kernels):
+                  kernels, n_valid: int | None = None):
     """One rank's backward pass.  Returns (dq, dk, dv) in q's dtype."""
     B, n, H, D = q.shape
     G, r = transport.world, transport.rank
@@ -305,7 +307,7 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
     cur_k, cur_v = k, v
     spare = None
     for h in range(G):
-        plan = plan_hop(r, G, h, n, causal, zigzag)
+        plan = plan_hop(r, G, h, n, causal, zigzag, n_valid)
         ops = []
         if h < G - 1:
             if spare is None:
@@ -314,7 +316,7 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
                     (RECV, spare[0], (r - 1) % G), (RECV, spare[1], (r - 1) % G)]
         if h >= 2:
             p_ops, got = _part_exchange(r, G, n, causal, zigzag, h - 1, send[(h - 1) % 2],
-                                        kernels, k, v)
+                                        kernels, k, v, n_valid)
             ops += p_ops
             if got is not None:
                 received.append(got)
@@ -342,7 +344,7 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
                 spare = None
     if G > 1:
         p_ops, got = _part_exchange(r, G, n, causal, zigzag, G - 1, send[(G - 1) % 2], kernels,
-                                    k, v)
+                                    k, v, n_valid)
         if got is not None:
             received.append(got)
         S.comm_after_compute()

@@ -74,14 +74,35 @@ def source_rank(rank: int, world: int, hop: int) -> int:
     return (rank - hop) % world
 
 
+def valid_rows(rank: int, world: int, n_local: int, zigzag: bool, n_valid: int | None) -> int:
+    """Rows of a (zero-padded) shard holding real positions < n_valid; always a
+    prefix of the shard's local order (padding sits at the end of the sequence,
+    ring.py:111-115 / _pad_rows 130-133)."""
+    if n_valid is None:
+        return n_local
+    if not zigzag:
+        return max(0, min(n_local, n_valid - rank * n_local))
+    c = n_local // 2
+    first = max(0, min(c, n_valid - rank * c))
+    second = max(0, min(c, n_valid - (2 * world - 1 - rank) * c))
+    return first + (second if first == c else 0)
+
+
 def plan_hop(rank: int, world: int, hop: int, n_local: int, causal: bool,
-             zigzag: bool) -> HopPlan:
+             zigzag: bool, n_valid: int | None = None) -> HopPlan:
+    """Rectangle of one hop.  With padding (n_valid = real global length), padded
+    keys are excluded by shortening the key range (BlockMask.with_padding,
+    masking.py:74-75); under the causal rule they are invisible to every real
+    query anyway, since they sit after all real positions."""
     src = source_rank(rank, world, hop)
     qm = shard_map(rank, world, n_local, zigzag)
     km = shard_map(src, world, n_local, zigzag)
     n = n_local
     if not causal:
-        return HopPlan(hop, rank, src, FULL, 0, n, 0, n, False, qm, km)
+        kv = valid_rows(src, world, n_local, zigzag, n_valid)
+        if kv == 0 and hop > 0:
+            return HopPlan(hop, rank, src, SKIP, 0, 0, 0, 0, False, qm, km)
+        return HopPlan(hop, rank, src, FULL, 0, n, 0, kv, False, qm, km)
     if src == rank:
         return HopPlan(hop, rank, src, DIAG, 0, n, 0, n, True, qm, km)
     if zigzag:

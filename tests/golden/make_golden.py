@@ -36,13 +36,13 @@ def _checksum(arrs):
                     [float(a.reshape(-1)[7]) for a in arrs])
 
 
-def ring_case(name, seq, dim, heads, gpus, precision, mask=None, tile=None, seed=0):
+def ring_case(name, seq, dim, heads, gpus, precision, mask=None, tile=None, seed=0, pad=False):
     cfg = RunConfig(seq=seq, dim=dim, heads=heads, gpus=gpus, precision=precision,
-                    mask=mask, tile_rows=tile, seed=seed)
+                    mask=mask, tile_rows=tile, seed=seed, pad=pad)
     cfg.validate()
     problems, do = generate_inputs(cfg)
     tiles = TileSpec(tile, tile) if tile else None
-    cluster = build_cluster(problems, gpus, tiles)
+    cluster = build_cluster(problems, gpus, tiles, pad=pad)
     fwd = run_ring_pass(cluster, "forward")
     bwd = run_ring_pass(cluster, "backward", do_slices=do)
     out = {}
@@ -102,6 +102,10 @@ if __name__ == "__main__":
               tile=8, seed=2)
     ring_case("ring_n256_d64_h1_g2_causal_f32", 256, 64, 1, 2, "single", mask="causal",
               tile=64, seed=3)
+    # padding: seq not divisible by G (RunConfig.pad, ring.partition pad=True)
+    ring_case("ring_n100_d16_h2_g3_pad_f32", 100, 16, 2, 3, "single", tile=16, seed=4, pad=True)
+    ring_case("ring_n98_d16_h1_g4_causal_pad_f32", 98, 16, 1, 4, "single", mask="causal",
+              tile=16, seed=5, pad=True)
     # LAO rectangles in global coordinates (row/col offsets), causal partial tiles
     lao_case("lao_r12_c20_d8_causal", 12, 20, 8, 16, 4, 40, True, 7)
     lao_case("lao_r16_c16_d8_full", 16, 16, 8, 0, 16, 32, False, 8)

@@ -83,3 +83,34 @@ def test_c1_golden_fp32(golden):
         ref = g[key].transpose(1, 0, 2)[None]
         assert rel_err(got, ref) < 1e-5, key
     assert rel_err(res.lse, g["lse"][None]) < 1e-5
+
+
+@pytest.mark.parametrize("name,zigzag", [("ring_n100_d16_h2_g3_pad_f32", False),
+                                         ("ring_n98_d16_h1_g4_causal_pad_f32", False),
+                                         ("ring_n98_d16_h1_g4_causal_pad_f32", True)])
+def test_f32_padding_vs_reference_golden(golden, name, zigzag):
+    """Sequence not divisible by G, zero-padded (reference pad=True): the f32 CUDA
+    path against the reference's own outputs, <= 1e-5 relative."""
+    from oracle import burst_oracle as orc
+    from paper_2403_09347_b200 import run_ring_pass
+    g = golden(name)
+    seq, dim, heads, gpus, seed, causal, tile, prec = (int(x) for x in g["meta"])
+    qn, kn, vn, dn, scale = orc.generate_inputs(seq, dim, heads, 1, seed, np.float32)
+    to = lambda a: torch.from_numpy(np.ascontiguousarray(a.transpose(1, 0, 2)[None])).cuda()
+    res = run_ring_pass(to(qn), to(kn), to(vn), gpus, causal=bool(causal), dout=to(dn),
+                        zigzag=zigzag, pad=True)
+    torch.cuda.synchronize()
+    for key, got in (("o", res.out), ("dq", res.dq), ("dk", res.dk), ("dv", res.dv)):
+        assert rel_err(got, g[key].transpose(1, 0, 2)[None]) < 1e-5, key
+
+
+@pytest.mark.parametrize("N,world,causal", [(1000, 3, False), (1990, 2, True), (700, 4, False)])
+def test_bf16_padding(N, world, causal):
+    q, k, v, do = make_inputs(1, N, 2, 128, seed=N)
+    from paper_2403_09347_b200 import run_ring_pass
+    res = run_ring_pass(q, k, v, world, causal=causal, dout=do, pad=True)
+    torch.cuda.synchronize()
+    o, lse, dq, dk, dv = oracle_ring(q, k, v, do, 1, causal, False)
+    assert max_abs(res.out, o) < BF16_TOL and max_abs(res.lse, lse) < 1e-2
+    for got, ref in ((res.dq, dq), (res.dk, dk), (res.dv, dv)):
+        assert max_abs(got, ref) < BF16_TOL

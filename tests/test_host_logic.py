@@ -207,3 +207,45 @@ def test_engine_gloo_two_processes(causal, zigzag, tmp_path):
     N = 24 * world
     q, k, v, do = (torch.randn(1, N, 2, 8, generator=g, dtype=torch.float64) for _ in range(4))
     _check(res, q, k, v, do, causal)
+
+
+# ---------------------------------------------------------------- padding (reference pad=True)
+
+@pytest.mark.parametrize("name,zigzag", [("ring_n100_d16_h2_g3_pad_f32", False),
+                                         ("ring_n98_d16_h1_g4_causal_pad_f32", False),
+                                         ("ring_n98_d16_h1_g4_causal_pad_f32", True)])
+def test_engine_padding_matches_reference_golden(golden, name, zigzag):
+    """Non-divisible sequence, zero-padded (ring.partition pad=True, ring.py:111-115):
+    the engine's ring over oracle kernels must reproduce the reference's outputs."""
+    from paper_2403_09347_b200 import run_ring_pass
+    g = golden(name)
+    seq, dim, heads, gpus, seed, causal, tile, prec = (int(x) for x in g["meta"])
+    q, k, v, do, scale = orc.generate_inputs(seq, dim, heads, 1, seed, np.float64)
+    to = lambda a: torch.from_numpy(np.ascontiguousarray(a.transpose(1, 0, 2)[None]))
+    res = run_ring_pass(to(q), to(k), to(v), gpus, causal=bool(causal), dout=to(do),
+                        zigzag=zigzag, kernels=OracleKernels(), pad=True)
+    for key, got in (("o", res.out), ("dq", res.dq), ("dk", res.dk), ("dv", res.dv)):
+        ref = g[key].transpose(1, 0, 2)[None]
+        err = np.max(np.abs(got.numpy() - ref)) / np.max(np.abs(ref))
+        assert err < 1e-5, (key, err)
+    assert np.max(np.abs(res.lse.numpy() - g["lse"][None])) < 1e-5
+
+
+def test_padding_required_flag():
+    from paper_2403_09347_b200 import ConfigError, run_ring_pass
+    x = torch.zeros(1, 10, 1, 8, dtype=torch.float64)
+    with pytest.raises(ConfigError):
+        run_ring_pass(x, x, x, 4, kernels=OracleKernels())
+
+
+def test_valid_rows_is_prefix():
+    from paper_2403_09347_b200.schedule import shard_map, valid_rows
+    for G, n, nv in ((4, 26, 98), (3, 34, 100), (2, 10, 37)):
+        for zz in (False, True):
+            if zz and n % 2:
+                continue
+            for r in range(G):
+                pos = shard_map(r, G, n, zz).positions(n)
+                want = [p < nv for p in pos]
+                k = valid_rows(r, G, n, zz, nv)
+                assert want == [True] * k + [False] * (n - k)
