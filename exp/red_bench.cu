@@ -4,10 +4,11 @@
 //   mode 2: st.global.v4 (plain store, upper bound)
 // Each CTA reduces a 64 KB tile per round into a target region of `region_mb`.
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 
-__global__ void __launch_bounds__(128) k_red(float* dst, size_t region_floats, int rounds, int mode) {
+__global__ void __launch_bounds__(128) k_red(float* dst, size_t region_floats, int rounds, int mode, int groups) {
   extern __shared__ __align__(128) float sm[];   // 32 KB staging (2 x 16 KB)
   const int t = threadIdx.x;
   for (int i = t; i < 8192; i += 128) sm[i] = 1.0f;
@@ -16,7 +17,8 @@ __global__ void __launch_bounds__(128) k_red(float* dst, size_t region_floats, i
   size_t tile = 16384;  // floats per 64 KB tile
   size_t ntiles = region_floats / tile;
   for (int r = 0; r < rounds; ++r) {
-    size_t tidx = ((size_t)blockIdx.x * 7919 + (size_t)r * 131) % ntiles;
+    size_t tidx = groups <= 0 ? ((size_t)blockIdx.x * 7919 + (size_t)r * 131) % ntiles
+                            : ((size_t)r + (size_t)(blockIdx.x % groups) * (ntiles / groups)) % ntiles;
     float* base = dst + tidx * tile;
     if (mode == 0) {
 #pragma unroll 4
@@ -44,8 +46,10 @@ __global__ void __launch_bounds__(128) k_red(float* dst, size_t region_floats, i
   if (mode == 1 && t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-int main() {
-  size_t region_mb = 256;
+int main(int argc, char** argv) {
+  size_t region_mb = argc > 1 ? (size_t)atoi(argv[1]) : 256;
+  int groups = argc > 2 ? atoi(argv[2]) : 0;
+  printf("region %zu MB, groups %d (0 = scattered; g = CTAs in g lockstep groups)\n", region_mb, groups);
   size_t nf = region_mb * 1024 * 1024 / 4;
   float* d;
   cudaMalloc(&d, nf * 4);
@@ -55,11 +59,11 @@ int main() {
   for (int ctas_per_sm = 1; ctas_per_sm <= 2; ++ctas_per_sm)
     for (int mode = 0; mode < 3; ++mode) {
       int grid = 148 * ctas_per_sm, rounds = 400;
-      k_red<<<grid, 128, 32768>>>(d, nf, 10, mode);
+      k_red<<<grid, 128, 32768>>>(d, nf, 10, mode, groups);
       cudaEvent_t a, b;
       cudaEventCreate(&a); cudaEventCreate(&b);
       cudaEventRecord(a);
-      k_red<<<grid, 128, 32768>>>(d, nf, rounds, mode);
+      k_red<<<grid, 128, 32768>>>(d, nf, rounds, mode, groups);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       float ms;

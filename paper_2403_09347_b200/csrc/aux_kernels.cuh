@@ -130,5 +130,22 @@ __global__ void bwd_finalize_kernel(int B, int H, int D, int64_t n, const float*
   }
 }
 
+// Zero the rows of a TL contribution buffer outside [lo, hi): a hop's LAO-bwd
+// writes (accumulate = 0) only the visiting key rows it covers, so a partial
+// key range (K_EARLY_HALF, padded shards) leaves the rest to this kernel.
+__global__ void zero_rows_outside_kernel(int B, int H, int D, int64_t n, int64_t lo, int64_t hi,
+                                         float* __restrict__ a, float* __restrict__ b) {
+  const int64_t NT = ceil_div(n, 128);
+  const int64_t total = (int64_t)B * H * NT * (D / 4) * 128;
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = (((i >> 7) / (D / 4)) % NT) * 128 + (i & 127);
+    if (row >= lo && row < hi) continue;
+    if (a) reinterpret_cast<float4*>(a)[i] = z;
+    if (b) reinterpret_cast<float4*>(b)[i] = z;
+  }
+}
+
 }  // namespace aux
 }  // namespace burst

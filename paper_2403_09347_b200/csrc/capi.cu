@@ -14,6 +14,7 @@
 #include "aux_kernels.cuh"
 #include "lao_bwd2_sm100.cuh"
 #include "lao_bwd3_sm100.cuh"
+#include "lao_bwd4_sm100.cuh"
 #include "lao_bwd_sm100.cuh"
 #include "lao_fwd_sm100.cuh"
 #include "simt_f32.cuh"
@@ -230,11 +231,12 @@ int launch_bwd2_bf16(const burst_hop* h, const void* q, const void* k, const voi
 }
 
 // Backward kernel variant for bf16 (BURST_BWD_KERNEL: 1 = single CTA + red.global,
-// 2 = CTA pair, 3 = single CTA + SMEM-staged TMA bulk reductions; default 3).
+// 2 = CTA pair, 3 = single CTA + SMEM-staged TMA bulk reductions, 4 = variant 3 with two
+// P/dS warpgroups and a double-buffered dQ drain; default 4).
 int bwd_variant() {
   static int v = [] {
     const char* e = getenv("BURST_BWD_KERNEL");
-    return (e && e[0] >= '1' && e[0] <= '3') ? e[0] - '0' : 3;
+    return (e && e[0] >= '1' && e[0] <= '4') ? e[0] - '0' : 4;
   }();
   return v;
 }
@@ -263,6 +265,34 @@ int launch_bwd3_bf16(const burst_hop* h, const void* q, const void* k, const voi
   if (attr_rc) return attr_rc;
   dim3 grid((unsigned)ceil_div(h->k_len, bwd3::BN), h->heads, h->batch);
   bwd3::lao_bwd3_kernel<D><<<grid, bwd3::kThreads, bwd3::Cfg<D>::kSmemBytes, st>>>(p);
+  CHECK_LAUNCH();
+  return BURST_OK;
+}
+
+template <int D>
+int launch_bwd4_bf16(const burst_hop* h, const void* q, const void* k, const void* v, const void* dout,
+                     const float* stats, float* dq_acc, float* dk, float* dv, int acc, cudaStream_t st) {
+  bwd4::Params p;
+  memset(&p, 0, sizeof(p));
+  int rc;
+  if ((rc = make_tmap(&p.tm_q, q, h->n_q, h->heads, D, h->batch))) return rc;
+  if ((rc = make_tmap(&p.tm_do, dout, h->n_q, h->heads, D, h->batch))) return rc;
+  if ((rc = make_tmap(&p.tm_k, k, h->n_k, h->heads, D, h->batch))) return rc;
+  if ((rc = make_tmap(&p.tm_v, v, h->n_k, h->heads, D, h->batch))) return rc;
+  p.stats = stats; p.dq_acc = dq_acc; p.dk_acc = dk; p.dv_acc = dv;
+  p.hop = *h;
+  p.scale_log2 = h->softmax_scale * kLog2e;
+  p.scale = h->softmax_scale;
+  p.accumulate = acc;
+#ifdef BURST_TRACE
+  p.trace = trace_buffer();
+#endif
+  static std::once_flag once;
+  static int attr_rc = 0;
+  std::call_once(once, [] { attr_rc = set_smem(bwd4::lao_bwd4_kernel<D>, bwd4::Cfg<D>::kSmemBytes); });
+  if (attr_rc) return attr_rc;
+  dim3 grid((unsigned)ceil_div(h->k_len, bwd4::BN), h->heads, h->batch);
+  bwd4::lao_bwd4_kernel<D><<<grid, bwd4::kThreads, bwd4::Cfg<D>::kSmemBytes, st>>>(p);
   CHECK_LAUNCH();
   return BURST_OK;
 }
@@ -388,17 +418,29 @@ int burst_lao_bwd(const burst_hop* hop, const void* q, const void* k, const void
   int rc = check_hop(hop);
   if (rc) return rc;
   if (!stats) return fail(BURST_E_ORDER, "backward needs the preprocess stats (forward lse, D)");
-  if (hop->k_len == 0) return BURST_OK;
   cudaStream_t st = (cudaStream_t)stream;
+  if (!accumulate && (hop->k_begin > 0 || hop->k_begin + hop->k_len < hop->n_k)) {
+    // accumulate = 0 defines the whole contribution buffer: rows the hop does not
+    // cover are zero (their sum in burst_bwd_finalize must not see stale memory)
+    const int64_t work = (int64_t)burst_workspace_floats(hop->batch, hop->heads, hop->head_dim,
+                                                         hop->n_k) / 4;
+    aux::zero_rows_outside_kernel<<<grid_for(work, 256), 256, 0, st>>>(
+        hop->batch, hop->heads, hop->head_dim, hop->n_k, hop->k_begin, hop->k_begin + hop->k_len,
+        dk_acc, dv_acc);
+    CHECK_LAUNCH();
+  }
+  if (hop->k_len == 0) return BURST_OK;
   if (hop->dtype == BURST_DTYPE_BF16) {
     // the staged kernel reduces whole 128-row TL tiles: needs 128-aligned query ranges
-    const int var = (bwd_variant() == 3 && hop->q_begin % 128 != 0) ? 1 : bwd_variant();
+    const int var = (bwd_variant() >= 3 && hop->q_begin % 128 != 0) ? 1 : bwd_variant();
     if (hop->head_dim == 128) {
       if (var == 2) return launch_bwd2_bf16(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
       if (var == 3) return launch_bwd3_bf16<128>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
+      if (var == 4) return launch_bwd4_bf16<128>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
       return launch_bwd_bf16<128>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
     }
     if (var == 3) return launch_bwd3_bf16<64>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
+    if (var == 4) return launch_bwd4_bf16<64>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
     return launch_bwd_bf16<64>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
   }
   switch (hop->head_dim) {

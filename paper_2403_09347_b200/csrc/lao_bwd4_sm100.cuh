@@ -1,39 +1,43 @@
-// LAO backward on sm_100a, K/V-stationary, dQ drained through SMEM with TMA bulk
-// reductions (cp.reduce.async.bulk) instead of per-thread red.global: the LSU
-// reduction stream was measured to starve the shared-memory MMA operands
-// (exp/trace_bwd.py).  dO is single-buffered (reloaded as soon as dV retires) to
-// free the 32 KB staging buffer.  Otherwise identical to lao_bwd_sm100.cuh.
-//
-// LAO backward on sm_100a, K/V-stationary.
+// LAO backward on sm_100a, K/V-stationary, 16 warps: the P/dS work of a
+// 128-key x 128-query step is split by query half over TWO warpgroups.
 //
 // Reference semantics: one call = ring.backward_step (ring.py:221-242) for every
 // (batch, head) slice, i.e. local_backward (local_attn.py:255-289, tiled form
 // _backward_tiled 313-353) over the hop's rectangle:
 //     P = exp(S - lse); dV += P^T dO; dP = dO V^T; dS = P * (dP - D);
 //     dQ += scale dS K;  dK += scale dS^T Q
-// computed transposed per key tile (S^T = K Q^T), so the visiting block's dK/dV
-// accumulate in TMEM across all query tiles and dQ (pinned on this rank) is
-// reduced into an fp32 workspace with vector atomics.
+// computed transposed per key tile (S^T = K Q^T): the visiting block's dK/dV
+// accumulate in TMEM across all query tiles, dQ (pinned on this rank) is reduced
+// into an fp32 workspace with TMA bulk reductions.
+//
+// Why this shape (measured on lao_bwd3, exp/trace_bwd.py): with ONE P/dS
+// warpgroup (one warp per SM sub-partition) the exp phase took ~2000 cycles and
+// the dS phase ~1000 of a ~4800-cycle step, both on the MMA dependency chain.
+// Two warpgroups (two warps per sub-partition, 64 query columns each) halve both
+// phases; the dQ drain double-buffers its SMEM staging in 16 KB quarters so the
+// staging writes overlap the bulk reduction reads; the MMA issuer no longer
+// blocks dK/dQ behind a late Q_{i+1} load.
 //
 // CTA = one key tile of 128 rows (K, V stationary in SMEM); loops over the
-// hop's query tiles of 128 (Q_i, dO_i, lse_i, D_i double-buffered by TMA).
-//   warps 0-3  P / dS warpgroup (thread = key row = TMEM lane); dK/dV epilogue
-//   warps 4-7  dQ drain warpgroup (thread = query row of the dQ tile)
-//   warp  8    TMA producer (+ TMEM allocator)
-//   warp  9    tcgen05.mma issuer
-// TMEM (512 cols for D=128): S^T [0,128) (P^T bf16 in [0,64)), dP^T [128,256)
-// (then dQ_i once dS_i is built), dV [256,256+D), dK [256+D,256+2D).
+// hop's query tiles of 128 (Q_i + lse/D double-buffered, dO_i single-buffered).
+//   warps 0-3   P/dS, query columns [0,64)   (thread = key row = TMEM lane); dV epilogue
+//   warps 4-7   P/dS, query columns [64,128)                                ; dK epilogue
+//   warps 8-11  dQ drain (thread = query row of the dQ tile)
+//   warp  12    TMA producer (+ TMEM allocator);  warp 13 tcgen05.mma issuer
+// TMEM (512 cols for D=128): S^T [0,128) with P^T (bf16) of query half h written
+// over S^T columns [64h, 64h+32) by the warpgroup that read them; dP^T [128,256)
+// (then dQ_i once dS_i is built); dV [256,256+D); dK [256+D,256+2D).
 #pragma once
 #include <cuda.h>
 #include "common.cuh"
 #include "ptx.cuh"
 
 namespace burst {
-namespace bwd3 {
+namespace bwd4 {
 
 constexpr int BM = 128;  // query rows per iteration
 constexpr int BN = 128;  // key rows per CTA
-constexpr int kThreads = 384;   // 3 warpgroups (warps 10-11 idle) for setmaxnreg
+constexpr int kThreads = 512;
 
 template <int D>
 struct Cfg {
@@ -42,9 +46,9 @@ struct Cfg {
   static constexpr int kTileBytes = kBoxBytes * kBoxes;    // K, V, Q_i, dO_i tiles
   static constexpr int kDsBytes = BN * BM * 2;              // dS^T tile (bf16)
   static constexpr int kStatBytes = 2 * BM * 4;             // lse2_i, D_i
-  static constexpr int kStageBytes = BM * 64 * 4;            // dQ staging: 64 columns
+  static constexpr int kQuarterBytes = BM * 32 * 4;         // dQ staging: 32 columns
   static constexpr int kPayload = 2 * kTileBytes + 2 * kTileBytes + kTileBytes + kDsBytes +
-                                  kStageBytes + 2 * kStatBytes;
+                                  2 * kQuarterBytes + 2 * kStatBytes;
   static constexpr int kBarBytes = 128;
   static constexpr int kMaxSmem = 232448;
   static constexpr int kSmemBytes =
@@ -72,20 +76,19 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
-
 #ifdef BURST_TRACE
-#define BTRACE(ev, i)                                                                        \
+#define BTRACE4(ev, i)                                                                       \
   do {                                                                                       \
     if (p.trace && (blockIdx.x == 0 || blockIdx.x == 77) && blockIdx.y == 0 && blockIdx.z == 0 && \
         (i) < 64)                                                                            \
       p.trace[((blockIdx.x ? 16 : 0) + (ev)) * 64 + (i)] = clock64();                        \
   } while (0)
 #else
-#define BTRACE(ev, i)
+#define BTRACE4(ev, i)
 #endif
 
 template <int D>
-__global__ void __launch_bounds__(kThreads, 1) lao_bwd3_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_constant__ Params p) {
   using C = Cfg<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem;
@@ -100,8 +103,8 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd3_kernel(const __grid_cons
   uint8_t* sQ = sV + C::kTileBytes;            // [2] stages
   uint8_t* sdO = sQ + 2 * C::kTileBytes;       // single buffer
   uint8_t* sdS = sdO + C::kTileBytes;
-  float* sStage = reinterpret_cast<float*>(sdS + C::kDsBytes);  // dQ staging [16][128] float4
-  float* sStat = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(sStage) + C::kStageBytes);
+  float* sStage = reinterpret_cast<float*>(sdS + C::kDsBytes);  // [2] x [8][128] float4
+  float* sStat = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(sStage) + 2 * C::kQuarterBytes);
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sStat) + 2 * C::kStatBytes);
   uint64_t* kv_full = bars;
   uint64_t* qdo_full = bars + 1;   // [2]
@@ -136,22 +139,13 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd3_kernel(const __grid_cons
     if (first_q > qs) qs = hp.q_begin + ((first_q - hp.q_begin) / BM) * BM;
   }
   const int nq = qs < q_end ? (int)ceil_div(q_end - qs, BM) : 0;
-  // Query-tile visiting order is rotated per CTA: concurrently resident CTAs (consecutive
-  // key tiles of one head) then reduce into different dQ tiles instead of all hitting
-  // the same 64 KB of dQ_acc at once (L2 atomic hot spot).
-#ifndef BURST_EXP_ROT
-#define BURST_EXP_ROT 0
-#endif
-#if BURST_EXP_ROT == 0
+  // Query-tile order rotated per CTA: concurrently resident CTAs (consecutive key
+  // tiles of one head) reduce into different dQ tiles (measured best at 128K,
+  // profiles/r01_rotation_exp.txt).
   const int rot = nq > 0 ? (int)((blockIdx.x * 7u) % (unsigned)nq) : 0;
-#elif BURST_EXP_ROT == 1
-  const int rot = 0;
-#else
-  const int rot = nq > 0 ? (int)(((blockIdx.x % BURST_EXP_ROT) * (unsigned)nq / BURST_EXP_ROT) % (unsigned)nq) : 0;
-#endif
   auto qtile = [&](int i) -> int64_t { int j = i + rot; if (j >= nq) j -= nq; return qs + (int64_t)j * BM; };
 
-  if (warp == 8) {
+  if (warp == 12) {
     if (lane == 0) {
       ptx::mbar_init(kv_full, 1);
       for (int s = 0; s < 2; ++s) {
@@ -159,8 +153,8 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd3_kernel(const __grid_cons
         ptx::mbar_init(qdo_empty + s, 1);
       }
       ptx::mbar_init(s_full, 1);
-      ptx::mbar_init(p_full, BN);
-      ptx::mbar_init(ds_full, BN);
+      ptx::mbar_init(p_full, 2 * BN);
+      ptx::mbar_init(ds_full, 2 * BN);
       ptx::mbar_init(ds_empty, 1);
       ptx::mbar_init(dq_full, 1);
       ptx::mbar_init(dq_empty, BM);
@@ -182,9 +176,9 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd3_kernel(const __grid_cons
   ptx::tc_fence_after();
   const uint32_t tbase = *tmem_holder;
   constexpr uint32_t kS = 0, kDP = 128, kDV = 256, kDK = 256 + D;
-  if (warp >= 8) {
-   ptx::regs_dec<88>();
-   if (warp == 8) {
+  if (warp >= 12) {
+   ptx::regs_dec<80>();
+   if (warp == 12) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0 && nq > 0) {
       ptx::mbar_expect_tx(kv_full, 2 * C::kTileBytes);
@@ -192,7 +186,6 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd3_kernel(const __grid_cons
         ptx::tma_load_4d(sK + x * C::kBoxBytes, &p.tm_k, kv_full, x * 64, h, (int)k0, b);
         ptx::tma_load_4d(sV + x * C::kBoxBytes, &p.tm_v, kv_full, x * 64, h, (int)k0, b);
       }
-      // Q_i (+ lse/D stats) double-buffered; dO_i single-buffered, refilled when dV retires
       auto load_q = [&](int j) {
         const int s = j & 1;
         const int64_t q0 = qtile(j);
@@ -220,10 +213,11 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd3_kernel(const __grid_cons
         if (i + 2 < nq) load_q(i + 2);
       }
     }
-  } else if (warp == 9) {
+   } else if (warp == 13) {
     // ------------------------------------------------------------ MMA issuer
-    // Order per query tile i (steady state):
-    //   dV_i | S^T_{i+1} (overlaps dS_i) | dK_i, dQ_i -> dP region | dP^T_{i+1} (after dQ_i drained)
+    // Per query tile i: dV_i | {S^T_{i+1}, dK_i + dQ_i -> dP region} in whichever
+    // order their inputs arrive (S^T first when both are ready) | dP^T_{i+1} once
+    // dQ_i has been drained to registers.
     if (lane == 0 && nq > 0) {
       constexpr uint32_t id_kk = ptx::make_idesc_bf16(BN, BM, 0, 0);   // S^T, dP^T
       constexpr uint32_t id_kmn = ptx::make_idesc_bf16(BN, D, 0, 1);   // dV, dK (B MN-major)
@@ -238,47 +232,19 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd3_kernel(const __grid_cons
           ptx::mma_ss(tbase + kS, ptx::make_sdesc(aK + off, 0, 1024),
                       ptx::make_sdesc(q + off, 0, 1024), id_kk, kk > 0);
         }
+        ptx::mma_commit(s_full);
       };
-      auto dpt_mma = [&](int) {  // dP^T = V dO^T
-        const uint32_t dO = adO;
+      auto dpt_mma = [&]() {  // dP^T = V dO^T
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * C::kBoxBytes + (kk & 3) * 32;
           ptx::mma_ss(tbase + kDP, ptx::make_sdesc(aV + off, 0, 1024),
-                      ptx::make_sdesc(dO + off, 0, 1024), id_kk, kk > 0);
+                      ptx::make_sdesc(adO + off, 0, 1024), id_kk, kk > 0);
         }
+        ptx::mma_commit(dp_full);
       };
-      ptx::mbar_wait(kv_full, 0);
-      ptx::mbar_wait(qdo_full + 0, 0);
-      ptx::tc_fence_after();
-      st_mma(0);
-      ptx::mma_commit(s_full);
-      ptx::mbar_wait(do_full, 0);
-      ptx::tc_fence_after();
-      dpt_mma(0);
-      ptx::mma_commit(dp_full);
-      for (int i = 0; i < nq; ++i) {
-        const int s = i & 1;
-        const bool more = i + 1 < nq;
-        const uint32_t q = aQ + s * C::kTileBytes, dO = adO;
-        // dV += P^T dO   (A = P^T from TMEM, B = dO MN-major, reduction over queries)
-        ptx::mbar_wait(p_full, i & 1); BTRACE(0, i);
-        ptx::tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < BM / 16; ++kk)
-          ptx::mma_ts(tbase + kDV, tbase + kS + kk * 8,
-                      ptx::make_sdesc(dO + kk * 2048, C::kBoxBytes, 1024), id_kmn,
-                      (i > 0 || kk > 0) ? 1u : 0u);
-        ptx::mma_commit(do_empty);
-        if (more) {
-          ptx::mbar_wait(qdo_full + (s ^ 1), ((i + 1) >> 1) & 1); BTRACE(11, i);
-          ptx::tc_fence_after();
-          st_mma(s ^ 1);
-          ptx::mma_commit(s_full);
-        }
-        // dK += dS^T Q ; dQ_i = dS K  (into the dP^T columns, already consumed)
-        ptx::mbar_wait(ds_full, i & 1); BTRACE(1, i);
-        ptx::tc_fence_after();
+      auto dkq_mma = [&](int i) {   // dK += dS^T Q ; dQ_i = dS K (into the drained dP^T columns)
+        const uint32_t q = aQ + (i & 1) * C::kTileBytes;
 #pragma unroll
         for (int kk = 0; kk < BM / 16; ++kk) {
           const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
@@ -292,22 +258,57 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd3_kernel(const __grid_cons
                       ptx::make_sdesc(aK + kk * 2048, C::kBoxBytes, 1024), id_mnmn, kk > 0);
         ptx::mma_commit(dq_full);
         ptx::mma_commit(ds_empty);
-        ptx::mma_commit(qdo_empty + s);
+        ptx::mma_commit(qdo_empty + (i & 1));
+      };
+      ptx::mbar_wait(kv_full, 0);
+      ptx::mbar_wait(qdo_full + 0, 0);
+      ptx::tc_fence_after();
+      st_mma(0);
+      ptx::mbar_wait(do_full, 0);
+      ptx::tc_fence_after();
+      dpt_mma();
+      for (int i = 0; i < nq; ++i) {
+        const int s = i & 1;
+        const bool more = i + 1 < nq;
+        // dV += P^T dO   (A = P^T from TMEM: query half h at S^T columns [64h, 64h+32))
+        ptx::mbar_wait(p_full, i & 1); BTRACE4(0, i);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < BM / 16; ++kk)
+          ptx::mma_ts(tbase + kDV, tbase + kS + (kk < 4 ? kk * 8 : 32 + kk * 8),
+                      ptx::make_sdesc(adO + kk * 2048, C::kBoxBytes, 1024), id_kmn,
+                      (i > 0 || kk > 0) ? 1u : 0u);
+        ptx::mma_commit(do_empty);
+        bool st_done = !more, dkq_done = false;
+        while (!st_done || !dkq_done) {
+          if (!st_done && ptx::mbar_try_wait(qdo_full + (s ^ 1), ((i + 1) >> 1) & 1)) {
+            BTRACE4(11, i);
+            ptx::tc_fence_after();
+            st_mma(s ^ 1);
+            st_done = true;
+          }
+          if (!dkq_done && ptx::mbar_try_wait(ds_full, i & 1)) {
+            BTRACE4(1, i);
+            ptx::tc_fence_after();
+            dkq_mma(i);
+            dkq_done = true;
+          }
+        }
         if (more) {
-          ptx::mbar_wait(dq_empty, i & 1); BTRACE(2, i);
-          ptx::mbar_wait(do_full, (i + 1) & 1); BTRACE(10, i);
+          ptx::mbar_wait(dq_empty, i & 1); BTRACE4(2, i);
+          ptx::mbar_wait(do_full, (i + 1) & 1); BTRACE4(10, i);
           ptx::tc_fence_after();
-          dpt_mma(s ^ 1);
-          ptx::mma_commit(dp_full);
+          dpt_mma();
         }
       }
       ptx::mma_commit(dkv_full);
     }
    }
-  } else if (warp < 4) {
-    // ------------------------------------------------------------ P / dS warpgroup
-    ptx::regs_inc<240>();
-    const int t = threadIdx.x;                  // key row within the tile
+  } else if (warp < 8) {
+    // ------------------------------------------------------------ P / dS, query half hq
+    ptx::regs_inc<144>();
+    const int hq = warp >> 2;                   // query columns [64 hq, 64 hq + 64)
+    const int t = threadIdx.x & 127;            // key row within the tile
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const int64_t krow = k0 + t;
     const bool kvalid = krow < k_end && krow < hp.n_k;
@@ -316,27 +317,26 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd3_kernel(const __grid_cons
     const float c2 = p.scale_log2;
     for (int i = 0; i < nq; ++i) {
       const int s = i & 1;
-      const int64_t q0 = qtile(i);
-      // visible query columns of this key row: [lo, hi)
+      const int64_t q0 = qtile(i) + 64 * hq;
+      // visible query columns of this key row within the half: [lo, hi)
       int64_t lo64 = qfirst - q0, hi64 = q_end - q0;
-      const int lo = lo64 < 0 ? 0 : (lo64 > BM ? BM : (int)lo64);
-      const int hi = !kvalid ? 0 : (hi64 > BM ? BM : (hi64 < 0 ? 0 : (int)hi64));
-      const bool warp_full = __all_sync(0xffffffffu, lo == 0 && hi == BM);
+      const int lo = lo64 < 0 ? 0 : (lo64 > 64 ? 64 : (int)lo64);
+      const int hi = !kvalid ? 0 : (hi64 > 64 ? 64 : (hi64 < 0 ? 0 : (int)hi64));
+      const bool warp_full = __all_sync(0xffffffffu, lo == 0 && hi == 64);
       ptx::mbar_wait(qdo_full + s, (i >> 1) & 1);
-      ptx::mbar_wait(s_full, i & 1); BTRACE(3, i);
+      ptx::mbar_wait(s_full, i & 1); if (hq == 0) BTRACE4(3, i);
       ptx::tc_fence_after();
-      const float4* lse4 = reinterpret_cast<const float4*>(sStat + s * 2 * BM);
+      const float4* lse4 = reinterpret_cast<const float4*>(sStat + s * 2 * BM) + 16 * hq;
       const float4* dst4 = lse4 + BM / 4;
-      float pr[BM];
+      float pr[64];
       {
-        uint32_t r[BM];
-#pragma unroll
-        for (int cc = 0; cc < BM / 32; ++cc)
-          ptx::tmem_ld32(tbase + lane_off + kS + cc * 32, *reinterpret_cast<uint32_t(*)[32]>(r + cc * 32));
+        uint32_t r[64];
+        ptx::tmem_ld32(tbase + lane_off + kS + 64 * hq, *reinterpret_cast<uint32_t(*)[32]>(r));
+        ptx::tmem_ld32(tbase + lane_off + kS + 64 * hq + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
         ptx::tmem_wait_ld();
         ptx::reg_fence(r);
 #pragma unroll
-        for (int c4 = 0; c4 < BM / 4; ++c4) {
+        for (int c4 = 0; c4 < 16; ++c4) {
           const float4 L = lse4[c4];
           pr[4 * c4 + 0] = ptx::ex2(fmaf(__uint_as_float(r[4 * c4 + 0]), c2, -L.x));
           pr[4 * c4 + 1] = ptx::ex2(fmaf(__uint_as_float(r[4 * c4 + 1]), c2, -L.y));
@@ -346,62 +346,60 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd3_kernel(const __grid_cons
       }
       if (!warp_full) {
 #pragma unroll
-        for (int c = 0; c < BM; ++c)
+        for (int c = 0; c < 64; ++c)
           if (c < lo || c >= hi) pr[c] = 0.f;
       }
-#pragma unroll
-      for (int cc = 0; cc < BM / 64; ++cc) {
+      {
         uint32_t pk[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) pk[j] = ptx::pack_bf16(pr[cc * 64 + 2 * j], pr[cc * 64 + 2 * j + 1]);
-        ptx::tmem_st32(tbase + lane_off + kS + cc * 32, pk);
+        for (int j = 0; j < 32; ++j) pk[j] = ptx::pack_bf16(pr[2 * j], pr[2 * j + 1]);
+        ptx::tmem_st32(tbase + lane_off + kS + 64 * hq, pk);
       }
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(p_full); BTRACE(4, i);
+      ptx::mbar_arrive(p_full); if (hq == 0) BTRACE4(4, i);
 
-      ptx::mbar_wait(dp_full, i & 1); BTRACE(5, i);
+      ptx::mbar_wait(dp_full, i & 1); if (hq == 0) BTRACE4(5, i);
       ptx::mbar_wait(ds_empty, (i & 1) ^ 1);
       ptx::tc_fence_after();
+      uint8_t* rowp = sdS + hq * 16384 + t * 128;   // SW128 K-major box of this query half
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        uint32_t r[64];
-        ptx::tmem_ld32(tbase + lane_off + kDP + half * 64, *reinterpret_cast<uint32_t(*)[32]>(r));
-        ptx::tmem_ld32(tbase + lane_off + kDP + half * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+      for (int qc = 0; qc < 2; ++qc) {
+        uint32_t r[32];
+        ptx::tmem_ld32(tbase + lane_off + kDP + 64 * hq + 32 * qc, r);
         ptx::tmem_wait_ld();
         ptx::reg_fence(r);
-        uint32_t pk[32];
+        uint32_t pk[16];
 #pragma unroll
-        for (int j4 = 0; j4 < 16; ++j4) {
-          const float4 Dv = dst4[half * 16 + j4];
-          const int c = half * 64 + 4 * j4;
+        for (int j4 = 0; j4 < 8; ++j4) {
+          const float4 Dv = dst4[qc * 8 + j4];
+          const int c = qc * 32 + 4 * j4;
           pk[2 * j4] = ptx::pack_bf16(pr[c] * (__uint_as_float(r[4 * j4]) - Dv.x),
                                       pr[c + 1] * (__uint_as_float(r[4 * j4 + 1]) - Dv.y));
           pk[2 * j4 + 1] = ptx::pack_bf16(pr[c + 2] * (__uint_as_float(r[4 * j4 + 2]) - Dv.z),
                                           pr[c + 3] * (__uint_as_float(r[4 * j4 + 3]) - Dv.w));
         }
-        // SW128 K-major: row t, 16-byte query chunk ch (8 bf16) of 128 B swizzle row
-        uint8_t* rowp = sdS + half * 16384 + t * 128;
 #pragma unroll
-        for (int ch = 0; ch < 8; ++ch)
+        for (int u = 0; u < 4; ++u) {
+          const int ch = qc * 4 + u;   // 16-byte chunk (8 queries) of the 128 B swizzle row
           *reinterpret_cast<uint4*>(rowp + ((ch ^ (t & 7)) << 4)) =
-              make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
+              make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        }
       }
       ptx::fence_proxy_async_smem();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(ds_full); BTRACE(6, i);
+      ptx::mbar_arrive(ds_full); if (hq == 0) BTRACE4(6, i);
     }
     // -------------------------------------------------------- dK / dV epilogue
     if (nq > 0) {
       ptx::mbar_wait(dkv_full, 0);
       ptx::tc_fence_after();
     }
+    {
+      float* dst = hq == 0 ? p.dv_acc : p.dk_acc;
+      const float mul = hq == 0 ? 1.f : p.scale;
+      const uint32_t col0 = hq == 0 ? kDV : kDK;
 #pragma unroll 1
-    for (int which = 0; which < 2; ++which) {
-      float* dst = which == 0 ? p.dv_acc : p.dk_acc;
-      const float mul = which == 0 ? 1.f : p.scale;
-      const uint32_t col0 = which == 0 ? kDV : kDK;
-#pragma unroll
       for (int cc = 0; cc < D / 32; ++cc) {
         uint32_t r[32];
         if (nq > 0) {
@@ -426,20 +424,20 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd3_kernel(const __grid_cons
         }
       }
     }
-  } else if (warp < 8) {
-    // ------------------------------------------------------------ dQ drain warpgroup
-    // TMEM -> registers -> SMEM staging (64 columns at a time) -> one TMA bulk reduction
-    // per half tile into the TL workspace (each 64-column half of a 128-row tile is a
-    // contiguous 32 KB run there).
+  } else {
+    // ------------------------------------------------------------ dQ drain (warps 8-11)
+    // TMEM -> registers (whole tile, then dq_empty) -> SMEM staging in 32-column
+    // quarters (two 16 KB buffers) -> one TMA bulk reduction per quarter into the TL
+    // workspace (each quarter of a 128-row tile is a contiguous 16 KB run there).
+    ptx::regs_inc<144>();
     const int t = threadIdx.x & 127;           // query row within the tile
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     float4* stg = reinterpret_cast<float4*>(sStage);
     for (int i = 0; i < nq; ++i) {
       const int64_t q0 = qtile(i);
       const bool qvalid = q0 + t < q_end && q0 + t < hp.n_q;
-      ptx::mbar_wait(dq_full, i & 1); BTRACE(7, i);
+      ptx::mbar_wait(dq_full, i & 1); BTRACE4(7, i);
       ptx::tc_fence_after();
-      // whole tile to registers first: TMEM is released before any staging work
       uint32_t r[D];
 #pragma unroll
       for (int cc = 0; cc < D / 32; ++cc)
@@ -447,26 +445,41 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd3_kernel(const __grid_cons
       ptx::tmem_wait_ld();
       ptx::reg_fence(r);
       ptx::tc_fence_before();
-      ptx::mbar_arrive(dq_empty); BTRACE(8, i);
+      ptx::mbar_arrive(dq_empty); BTRACE4(8, i);
       const float sc = qvalid ? p.scale : 0.f;
+#if defined(BURST_EXP_DQ_REDG)    // experiment: per-thread red.global from registers
+      if (qvalid) {
+        float* base = p.dq_acc + tl_index(bh, q0 + t, 0, D, NTq);
 #pragma unroll
-      for (int half = 0; half < D / 64; ++half) {
-        if (t == 0) ptx::bulk_wait_read_all();   // staging consumed by the previous reduction
+        for (int j = 0; j < D; j += 4)
+          ptx::red_add_v4(base + (size_t)(j >> 2) * 512, __uint_as_float(r[j]) * sc,
+                          __uint_as_float(r[j + 1]) * sc, __uint_as_float(r[j + 2]) * sc,
+                          __uint_as_float(r[j + 3]) * sc);
+      }
+      if (false)
+#elif defined(BURST_EXP_NO_DQ)     // experiment: no dQ traffic at all (upper bound)
+      if (false)
+#endif
+#pragma unroll
+      for (int qq = 0; qq < D / 32; ++qq) {
+        float4* buf = stg + (qq & 1) * (8 * 128);
+        if (t == 0) ptx::bulk_wait_read<1>();   // the reduction that last read this buffer
         ptx::named_bar_sync(1, 128);
 #pragma unroll
-        for (int g = 0; g < 16; ++g) {
-          const int c = half * 64 + 4 * g;
-          stg[g * 128 + t] = make_float4(__uint_as_float(r[c]) * sc, __uint_as_float(r[c + 1]) * sc,
+        for (int g = 0; g < 8; ++g) {
+          const int c = qq * 32 + 4 * g;
+          buf[g * 128 + t] = make_float4(__uint_as_float(r[c]) * sc, __uint_as_float(r[c + 1]) * sc,
                                          __uint_as_float(r[c + 2]) * sc, __uint_as_float(r[c + 3]) * sc);
         }
         ptx::fence_proxy_async_smem();
         ptx::named_bar_sync(1, 128);
         if (t == 0) {
-          ptx::bulk_reduce_add_f32(p.dq_acc + tl_index(bh, q0, half * 64, D, NTq), sStage,
-                                   C::kStageBytes);
-          ptx::bulk_commit(); BTRACE(9, i);
+          ptx::bulk_reduce_add_f32(p.dq_acc + tl_index(bh, q0, qq * 32, D, NTq), buf,
+                                   C::kQuarterBytes);
+          ptx::bulk_commit();
         }
       }
+      BTRACE4(9, i);
     }
     if (t == 0) ptx::bulk_wait_all();
   }
@@ -474,11 +487,11 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd3_kernel(const __grid_cons
   __syncwarp();
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 8) {
+  if (warp == 12) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tbase, 512);
   }
 }
 
-}  // namespace bwd3
+}  // namespace bwd4
 }  // namespace burst

@@ -54,3 +54,11 @@ def rel_err(a, b):
     """Per-tensor max|x - ref| / max|ref| (SURVEY.md 8(c) definition)."""
     b = np.asarray(b, np.float64)
     return max_abs(a, b) / max(float(np.max(np.abs(b))), 1e-30)
+
+
+def poison_allocator(nbytes=256 << 20):
+    """Fill, then free, a large block so the caching allocator hands out NaN-filled
+    memory to the next torch.empty calls: any buffer a kernel forgets to define
+    then shows up as NaN in the results instead of passing by luck."""
+    x = torch.full((nbytes // 4,), float("nan"), dtype=torch.float32, device="cuda")
+    del x

@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 import torch
 
-from gpu_utils import make_inputs, max_abs, oracle_ring, rel_err
+from gpu_utils import make_inputs, max_abs, oracle_ring, poison_allocator, rel_err
 
 pytestmark = pytest.mark.gpu
 
@@ -71,6 +71,34 @@ def test_f32_path_rel_1e5(N, D, world, causal):
         assert rel_err(got, ref) < 1e-5
 
 
+@pytest.mark.parametrize("N,D,world", [(416, 32, 2), (208, 16, 4)])
+def test_f32_zigzag_causal_rel_1e5(N, D, world):
+    """Zigzag causal on the f32 path: chunk sizes not a multiple of any tile, partial
+    key ranges (K_EARLY_HALF) and query ranges (Q_LATE_HALF); allocator poisoned
+    with NaN so an undefined contribution row cannot pass by luck."""
+    q, k, v, do = make_inputs(1, N, 2, D, seed=11, dtype=torch.float32)
+    poison_allocator()
+    res = _run(q, k, v, do, world, True, zigzag=True)
+    o, lse, dq, dk, dv = oracle_ring(q, k, v, do, world, True, True)
+    assert rel_err(res.out, o) < 1e-5
+    for got, ref in ((res.dq, dq), (res.dk, dk), (res.dv, dv)):
+        assert rel_err(got, ref) < 1e-5
+
+
+@pytest.mark.parametrize("N,world", [(800, 2), (1088, 4)])
+def test_bf16_zigzag_unaligned_chunks(N, world):
+    """bf16 zigzag with chunks of 200 / 136 rows (8- but not 128-aligned): boundary key
+    tiles, unaligned Q_LATE_HALF query starts, poisoned allocator."""
+    q, k, v, do = make_inputs(1, N, 2, 128, seed=5)
+    poison_allocator()
+    res = _run(q, k, v, do, world, True, zigzag=True)
+    o, lse, dq, dk, dv = oracle_ring(q, k, v, do, world, True, True)
+    assert max_abs(res.out, o) < BF16_TOL
+    assert max_abs(res.lse, lse) < 1e-2
+    for got, ref in ((res.dq, dq), (res.dk, dk), (res.dv, dv)):
+        assert max_abs(got, ref) < BF16_TOL
+
+
 def test_c1_golden_fp32(golden):
     """BASELINE configs[0] (seq 1024, d 64, 2 heads, G 2, fp32) against the
     reference's own outputs (tests/golden, produced by the reference)."""
@@ -97,6 +125,7 @@ def test_f32_padding_vs_reference_golden(golden, name, zigzag):
     seq, dim, heads, gpus, seed, causal, tile, prec = (int(x) for x in g["meta"])
     qn, kn, vn, dn, scale = orc.generate_inputs(seq, dim, heads, 1, seed, np.float32)
     to = lambda a: torch.from_numpy(np.ascontiguousarray(a.transpose(1, 0, 2)[None])).cuda()
+    poison_allocator()
     res = run_ring_pass(to(qn), to(kn), to(vn), gpus, causal=bool(causal), dout=to(dn),
                         zigzag=zigzag, pad=True)
     torch.cuda.synchronize()
