@@ -79,9 +79,8 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 #ifdef BURST_TRACE
 #define BTRACE4(ev, i)                                                                       \
   do {                                                                                       \
-    if (p.trace && (blockIdx.x == 0 || blockIdx.x == 77) && blockIdx.y == 0 && blockIdx.z == 0 && \
-        (i) < 64)                                                                            \
-      p.trace[((blockIdx.x ? 16 : 0) + (ev)) * 64 + (i)] = clock64();                        \
+    if (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (i) < 64)       \
+      p.trace[(ev) * 64 + (i)] = clock64();                                                  \
   } while (0)
 #else
 #define BTRACE4(ev, i)
@@ -178,6 +177,17 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
   constexpr uint32_t kS = 0, kDP = 128, kDV = 256, kDK = 256 + D;
   if (warp >= 12) {
    ptx::regs_dec<80>();
+#ifdef BURST_TRACE
+   if (warp == 14 && lane == 0 && blockIdx.x == 0) {
+     // observer: completion times of the MMA groups (tensor-pipe timeline)
+     for (int i = 0; i < nq && i < 64; ++i) {
+       ptx::mbar_wait(s_full, i & 1); BTRACE4(16, i);
+       ptx::mbar_wait(do_empty, i & 1); BTRACE4(17, i);     // dV_i done
+       ptx::mbar_wait(dq_full, i & 1); BTRACE4(18, i);      // dK_i, dQ_i done
+       if (i + 1 < nq) { ptx::mbar_wait(dp_full, (i + 1) & 1); BTRACE4(19, i); }   // dP^T_{i+1} done
+     }
+   }
+#endif
    if (warp == 12) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0 && nq > 0) {
@@ -335,6 +345,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
         ptx::tmem_ld32(tbase + lane_off + kS + 64 * hq + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
         ptx::tmem_wait_ld();
         ptx::reg_fence(r);
+        if (hq == 0) BTRACE4(12, i);
 #pragma unroll
         for (int c4 = 0; c4 < 16; ++c4) {
           const float4 L = lse4[c4];
@@ -353,11 +364,13 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
         uint32_t pk[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) pk[j] = ptx::pack_bf16(pr[2 * j], pr[2 * j + 1]);
+        if (hq == 0) BTRACE4(13, i);
         ptx::tmem_st32(tbase + lane_off + kS + 64 * hq, pk);
       }
       ptx::tmem_wait_st();
+      if (hq == 0) BTRACE4(14, i);
       ptx::tc_fence_before();
-      ptx::mbar_arrive(p_full); if (hq == 0) BTRACE4(4, i);
+      ptx::mbar_arrive(p_full); if (hq == 0) BTRACE4(4, i); else BTRACE4(22, i);
 
       ptx::mbar_wait(dp_full, i & 1); if (hq == 0) BTRACE4(5, i);
       ptx::mbar_wait(ds_empty, (i & 1) ^ 1);
@@ -369,6 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
         ptx::tmem_ld32(tbase + lane_off + kDP + 64 * hq + 32 * qc, r);
         ptx::tmem_wait_ld();
         ptx::reg_fence(r);
+        if (hq == 0 && qc == 0) BTRACE4(20, i);
         uint32_t pk[16];
 #pragma unroll
         for (int j4 = 0; j4 < 8; ++j4) {
@@ -379,6 +393,9 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
           pk[2 * j4 + 1] = ptx::pack_bf16(pr[c + 2] * (__uint_as_float(r[4 * j4 + 2]) - Dv.z),
                                           pr[c + 3] * (__uint_as_float(r[4 * j4 + 3]) - Dv.w));
         }
+#ifdef BURST_EXP_NO_DS_STS   // experiment: dS never reaches SMEM (wrong results)
+        if (pk[0] == 0x7f7f7f7fu)
+#endif
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int ch = qc * 4 + u;   // 16-byte chunk (8 queries) of the 128 B swizzle row
@@ -386,9 +403,10 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
               make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
         }
       }
+      if (hq == 0) BTRACE4(21, i);
       ptx::fence_proxy_async_smem();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(ds_full); if (hq == 0) BTRACE4(6, i);
+      ptx::mbar_arrive(ds_full); if (hq == 0) BTRACE4(6, i); else BTRACE4(23, i);
     }
     // -------------------------------------------------------- dK / dV epilogue
     if (nq > 0) {
@@ -465,6 +483,9 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
         float4* buf = stg + (qq & 1) * (8 * 128);
         if (t == 0) ptx::bulk_wait_read<1>();   // the reduction that last read this buffer
         ptx::named_bar_sync(1, 128);
+#ifdef BURST_EXP_NO_STAGE_STS   // experiment: staging never written (wrong results)
+        if (r[qq] == 0x7f7f7f7fu)
+#endif
 #pragma unroll
         for (int g = 0; g < 8; ++g) {
           const int c = qq * 32 + 4 * g;
