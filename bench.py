@@ -239,8 +239,9 @@ def run_ours(args, cfg, rank, world, local_rank):
     for t in (q, k, v):
         t.requires_grad_(True)
 
-    def step(qq, kk, vv, dd):
-        o, lse = burst_attn_func(qq, kk, vv, causal=causal, zigzag=zigzag, _kernels=kern)
+    def step(qq, kk, vv, dd, recorders=None):
+        o, lse = burst_attn_func(qq, kk, vv, causal=causal, zigzag=zigzag, _kernels=kern,
+                                 _recorders=recorders)
         grads = torch.autograd.grad(o, (qq, kk, vv), dd)
         return o, grads
 
@@ -282,6 +283,29 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     bwd_ms, bwd_fl = kstats("bwd")
     fwd_ms, fwd_fl = kstats("fwd")
+
+    # ---- one extra (untimed) traced step: measured hop timeline of every rank's
+    # comm and compute streams (trace.py, the reference's ScheduleTrace schema)
+    comm_trace = None
+    if world > 1:
+        from paper_2403_09347_b200.trace import PassRecorder, comm_summary
+        recs = (PassRecorder(rank), PassRecorder(rank))
+        step(q, k, v, do, recs)
+        torch.cuda.synchronize()
+        sf, sb = comm_summary(recs[0].events()), comm_summary(recs[1].events())
+        vals = torch.tensor([sf["send_us"], sf["hidden_us"], sb["send_us"], sb["hidden_us"]],
+                            device=dev, dtype=torch.float64)
+        allv = [torch.zeros_like(vals) for _ in range(world)]
+        dist.all_gather(allv, vals)
+        tot = torch.stack(allv).sum(0).tolist()
+        comm_trace = {"fwd_send_us_all_ranks": tot[0], "fwd_hidden_frac": tot[1] / max(tot[0], 1e-9),
+                      "bwd_send_us_all_ranks": tot[2], "bwd_hidden_frac": tot[3] / max(tot[2], 1e-9),
+                      "fwd_bytes_per_rank": recs[0].ledger.bytes_sent_forward,
+                      "bwd_bytes_per_rank": recs[1].ledger.bytes_sent_backward,
+                      "fwd_GBps_per_rank": recs[0].ledger.bytes_sent_forward
+                      / max(tot[0] / world, 1e-9) / 1e3,
+                      "bwd_GBps_per_rank": recs[1].ledger.bytes_sent_backward
+                      / max(tot[2] / world, 1e-9) / 1e3}
 
     # ---- e2e through the public API with pinned host buffers
     host = [t.detach().cpu().pin_memory() for t in (q, k, v, do)]
@@ -358,7 +382,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         from paper_2403_09347_b200.ring import ring_comm_bytes
         fb, bb = ring_comm_bytes(n, B, H, D, world, 2, causal, zigzag)
         comm = {"bytes_sent_per_rank_per_step": fb + bb,
-                "avg_GBps_over_step": (fb + bb) / (ms / 1e3) / 1e9}
+                "avg_GBps_over_step": (fb + bb) / (ms / 1e3) / 1e9,
+                "measured": comm_trace}
     line = {
         "metric": METRIC, "value": tokens, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,

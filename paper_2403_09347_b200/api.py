@@ -21,6 +21,7 @@ from .errors import ConfigError, ShapeError
 from .kernels import CudaKernels, check_qkv, default_scale
 from .ring import NcclTransport, SoloTransport, ring_backward, ring_forward, run_ranks
 from .schedule import shard, unshard
+from .trace import PassRecorder, PassTrace, merge
 
 _kernels = None
 _transports = {}
@@ -48,25 +49,27 @@ def _transport_for(group):
 
 class _BurstAttnFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, q, k, v, scale, causal, zigzag, transport, kernels, n_valid):
-        o, lse = ring_forward(q, k, v, scale, causal, zigzag, transport, kernels, n_valid)
+    def forward(ctx, q, k, v, scale, causal, zigzag, transport, kernels, n_valid, recorders):
+        rec_f, rec_b = recorders if recorders is not None else (None, None)
+        o, lse = ring_forward(q, k, v, scale, causal, zigzag, transport, kernels, n_valid,
+                              recorder=rec_f)
         ctx.save_for_backward(q, k, v, o, lse)
-        ctx.cfg = (scale, causal, zigzag, transport, kernels, n_valid)
+        ctx.cfg = (scale, causal, zigzag, transport, kernels, n_valid, rec_b)
         ctx.mark_non_differentiable(lse)
         return o, lse
 
     @staticmethod
     def backward(ctx, do, _dlse):
         q, k, v, o, lse = ctx.saved_tensors
-        scale, causal, zigzag, transport, kernels, n_valid = ctx.cfg
+        scale, causal, zigzag, transport, kernels, n_valid, rec_b = ctx.cfg
         dq, dk, dv = ring_backward(q, k, v, o, lse, do.contiguous(), scale, causal, zigzag,
-                                   transport, kernels, n_valid)
-        return dq, dk, dv, None, None, None, None, None, None
+                                   transport, kernels, n_valid, recorder=rec_b)
+        return dq, dk, dv, None, None, None, None, None, None, None
 
 
 def burst_attn_func(q, k, v, causal: bool = False, softmax_scale: float | None = None,
                     group=None, zigzag: bool | None = None, valid_len: int | None = None, *,
-                    _transport=None, _kernels=None):
+                    _transport=None, _kernels=None, _recorders=None):
     """BurstAttention over the ranks of `group` (NCCL ring over NVLink).
 
     q, k, v: [batch, n_local, heads, head_dim] shards of the global sequence
@@ -76,6 +79,8 @@ def burst_attn_func(q, k, v, causal: bool = False, softmax_scale: float | None =
     `valid_len`: real global sequence length when the shards were zero-padded to
     a multiple of G (2G for zigzag); padded keys are excluded, padded rows of the
     outputs are meaningless (the reference's pad=True, ring.py:111-115).
+    `_recorders`: optional (forward, backward) trace.PassRecorder pair that
+    records this rank's measured hop timeline and byte ledger.
     """
     check_qkv(q, k, v) if _kernels is None else None
     if q.shape[1] != k.shape[1]:
@@ -92,7 +97,7 @@ def burst_attn_func(q, k, v, causal: bool = False, softmax_scale: float | None =
     if valid_len is not None and not 0 < valid_len <= q.shape[1] * transport.world:
         raise ShapeError(f"valid_len={valid_len} outside (0, {q.shape[1] * transport.world}]")
     return _BurstAttnFn.apply(q, k, v, scale, bool(causal), bool(zigzag), transport, kernels,
-                              valid_len)
+                              valid_len, _recorders)
 
 
 @dataclass
@@ -103,17 +108,20 @@ class PassResult:
     dq: torch.Tensor | None = None
     dk: torch.Tensor | None = None
     dv: torch.Tensor | None = None
+    trace: object | None = None     # trace.PassTrace when run_ring_pass(trace=True)
 
 
 def run_ring_pass(q, k, v, world: int, causal: bool = False, softmax_scale: float | None = None,
                   dout=None, zigzag: bool | None = None, kernels=None,
-                  pad: bool = False) -> PassResult:
+                  pad: bool = False, trace: bool = False) -> PassResult:
     """Whole-ring forward (+ backward when `dout` is given) of GLOBAL tensors
     [batch, N, heads, head_dim] over `world` simulated devices on this GPU.
 
     Mirrors build_cluster + run_ring_pass (sim.py:366-383, 501-657) with the
     threaded executor: one thread per device, real CUDA kernels, device
-    copies for the ring hand-off.
+    copies for the ring hand-off.  `trace=True` also returns the measured
+    per-hop timeline and byte ledger of every device (`.trace`, a
+    trace.PassTrace in the reference's ScheduleTrace / CommLedger schema).
     """
     if world < 1:
         raise ConfigError(f"gpus must be a positive integer, got {world}")
@@ -143,22 +151,34 @@ def run_ring_pass(q, k, v, world: int, causal: bool = False, softmax_scale: floa
     shards = [[shard(t, r, world, zigzag) for r in range(world)] for t in (q, k, v)]
     do_sh = [shard(dout, r, world, zigzag) for r in range(world)] if dout is not None else None
 
+    rec_f = [PassRecorder(r) for r in range(world)] if trace else [None] * world
+    rec_b = [PassRecorder(r) for r in range(world)] if trace else [None] * world
+
     def one(rank, transport):
         qs, ks, vs = shards[0][rank], shards[1][rank], shards[2][rank]
-        o, lse = ring_forward(qs, ks, vs, scale, causal, zigzag, transport, kernels, n_valid)
+        o, lse = ring_forward(qs, ks, vs, scale, causal, zigzag, transport, kernels, n_valid,
+                              recorder=rec_f[rank])
         if do_sh is None:
             return o, lse, None
         g = ring_backward(qs, ks, vs, o, lse, do_sh[rank], scale, causal, zigzag, transport,
-                          kernels, n_valid)
+                          kernels, n_valid, recorder=rec_b[rank])
         return o, lse, g
 
     res = run_ranks(world, one)
+    ptrace = None
+    if trace:
+        for rf, rb in zip(rec_f, rec_b):
+            rf.ledger.elements_sent_backward = rb.ledger.elements_sent_backward
+            rf.ledger.bytes_sent_backward = rb.ledger.bytes_sent_backward
+            rf.ledger.ring_steps_backward = rb.ledger.ring_steps_backward
+        ptrace = PassTrace(forward=merge(rec_f), backward=merge(rec_b) if do_sh else [],
+                           ledgers=[rf.ledger for rf in rec_f])
     # _collect drops padded rows (sim.py:450-471)
     out = unshard([x[0] for x in res], zigzag, dim=1)[:, :N]
     lse = unshard([x[1] for x in res], zigzag, dim=2)[:, :, :N]
     if dout is None:
-        return PassResult(out, lse)
+        return PassResult(out, lse, trace=ptrace)
     dq = unshard([x[2][0] for x in res], zigzag, dim=1)[:, :N]
     dk = unshard([x[2][1] for x in res], zigzag, dim=1)[:, :N]
     dv = unshard([x[2][2] for x in res], zigzag, dim=1)[:, :N]
-    return PassResult(out, lse, dq, dk, dv)
+    return PassResult(out, lse, dq, dk, dv, trace=ptrace)

@@ -240,9 +240,10 @@ class LoopbackTransport:
 # ---------------------------------------------------------------------------
 
 def ring_forward(q, k, v, scale: float, causal: bool, zigzag: bool, transport, kernels,
-                 n_valid: int | None = None):
+                 n_valid: int | None = None, recorder=None):
     """One rank's forward pass.  Returns (O [B,n,H,D], lse [B,H,n] natural log).
-    `n_valid`: real global length when the shards are zero-padded (reference pad=True)."""
+    `n_valid`: real global length when the shards are zero-padded (reference pad=True).
+    `recorder`: optional trace.PassRecorder (measured timeline + ledger, sim.py:118-261)."""
     B, n, H, D = q.shape
     G, r = transport.world, transport.rank
     S = _Streams(q.device)
@@ -259,15 +260,25 @@ def ring_forward(q, k, v, scale: float, causal: bool, zigzag: bool, transport, k
             if spare is None:
                 spare = (torch.empty_like(k), torch.empty_like(v))
             S.comm_after_compute()
-            transport.sendrecv([(SEND, cur_k, (r + 1) % G), (SEND, cur_v, (r + 1) % G),
-                                (RECV, spare[0], (r - 1) % G), (RECV, spare[1], (r - 1) % G)],
-                               S.comm)
+            ops = [(SEND, cur_k, (r + 1) % G), (SEND, cur_v, (r + 1) % G),
+                   (RECV, spare[0], (r - 1) % G), (RECV, spare[1], (r - 1) % G)]
+            if recorder is not None:
+                recorder.count_send("forward", ops)
+                recorder.mark(h, "send_start", S.comm)
+            transport.sendrecv(ops, S.comm)
+            if recorder is not None:
+                recorder.mark(h, "send_end", S.comm)
+                recorder.mark(h, "recv_ready", S.comm)
             exchanged = True
+        if recorder is not None:
+            recorder.mark(h, "compute_start", S.compute)
         if not plan.skip:
             fin = h == G - 1 and plan.covers_all_queries(n)
             kernels.fwd(plan, q, cur_k, cur_v, scale, state, o, lse, first=(h == 0), finalize=fin,
                         stream=S.compute)
             finalized = finalized or fin
+        if recorder is not None:
+            recorder.mark(h, "compute_end", S.compute)
         if exchanged:
             S.compute_after_comm()
             (cur_k, cur_v), spare = spare, (cur_k, cur_v)
@@ -294,8 +305,9 @@ def _part_exchange(r: int, G: int, n: int, causal: bool, zigzag: bool, hop: int,
 
 
 def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: bool, transport,
-                  kernels, n_valid: int | None = None):
-    """One rank's backward pass.  Returns (dq, dk, dv) in q's dtype."""
+                  kernels, n_valid: int | None = None, recorder=None):
+    """One rank's backward pass.  Returns (dq, dk, dv) in q's dtype.
+    `recorder`: optional trace.PassRecorder (see ring_forward)."""
     B, n, H, D = q.shape
     G, r = transport.world, transport.rank
     S = _Streams(q.device)
@@ -326,7 +338,15 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
         slot = h < G - 1 or h >= 2
         if slot:
             S.comm_after_compute()
+            if recorder is not None:
+                recorder.count_send("backward", ops)
+                recorder.mark(h, "send_start", S.comm)
             transport.sendrecv(ops, S.comm)
+            if recorder is not None:
+                recorder.mark(h, "send_end", S.comm)
+                recorder.mark(h, "recv_ready", S.comm)
+        if recorder is not None:
+            recorder.mark(h, "compute_start", S.compute)
         if h == 0:
             target = own
         else:
@@ -336,6 +356,8 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
         if not plan.skip:
             kernels.bwd(plan, q, cur_k, cur_v, dout, scale, st, target[0], target[1],
                         accumulate=False, stream=S.compute)
+        if recorder is not None:
+            recorder.mark(h, "compute_end", S.compute)
         if slot:
             S.compute_after_comm()
         if h < G - 1:
@@ -348,7 +370,13 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
         if got is not None:
             received.append(got)
         S.comm_after_compute()
+        if recorder is not None:
+            recorder.count_send("backward", p_ops)
+            recorder.mark(G, "send_start", S.comm)
         transport.sendrecv(p_ops, S.comm)
+        if recorder is not None:
+            recorder.mark(G, "send_end", S.comm)
+            recorder.mark(G, "recv_ready", S.comm)
         S.compute_after_comm()
     parts_k = [own[0]] + [x[0] for x in received]
     parts_v = [own[1]] + [x[1] for x in received]
