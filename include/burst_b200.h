@@ -15,6 +15,7 @@
  *   burst_lao_bwd        local_attn.local_backward         (local_attn.py:255-289)
  *                        = ring.backward_step accumulation (ring.py:221-242)
  *   burst_bwd_finalize   sim._collect gradient assembly    (sim.py:450-471)
+ *   burst_tl_sum         same, for travelling-query dQ contributions (ring.py:65-83)
  *   burst_ring_*         sim.RingChannel send/recv, DoubleBuffer (sim.py:281-332)
  *
  * Tensor layouts (row-major, contiguous):
@@ -109,6 +110,13 @@ BURST_API int burst_bwd_finalize(int dtype, int batch, int heads, int head_dim, 
                        const float* dq_acc, const float* const* dk_parts,
                        const float* const* dv_parts, int nparts, void* dq, void* dk, void* dv,
                        void* stream);
+
+/* out = sum of nparts TL f32 buffers (TL f32 -> dtype [batch, n, heads, head_dim]).
+ * Assembles a gradient from per-hop contributions: the dQ contributions of the
+ * reference's travelling-query backward payload (ring.py:65-83, 221-242; sim._collect
+ * sim.py:450-471) when K/V/dK/dV stay pinned. */
+BURST_API int burst_tl_sum(int dtype, int batch, int heads, int head_dim, int64_t n,
+                 const float* const* parts, int nparts, void* out, void* stream);
 
 /* Non-zero device-side flags raised by kernels since the last call (bit 0: a
  * row with no visible key, bit 1: non-finite output).  Synchronises `stream`. */

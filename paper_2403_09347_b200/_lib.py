@@ -57,6 +57,8 @@ _SIGS = {
     "burst_bwd_finalize": ([_c_i32, _c_i32, _c_i32, _c_i32, _c_i64, _c_p,
                             ctypes.POINTER(_c_p), ctypes.POINTER(_c_p), _c_i32, _c_p, _c_p, _c_p,
                             _c_p], _c_i32),
+    "burst_tl_sum": ([_c_i32, _c_i32, _c_i32, _c_i32, _c_i64, ctypes.POINTER(_c_p), _c_i32, _c_p,
+                      _c_p], _c_i32),
     "burst_read_flags": ([_c_p, ctypes.POINTER(_c_i32)], _c_i32),
     "burst_ring_unique_id": ([_c_p], _c_i32),
     "burst_ring_create": ([_c_p, _c_i32, _c_i32, _c_i32, ctypes.POINTER(_c_p)], _c_i32),

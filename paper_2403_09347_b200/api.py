@@ -19,7 +19,8 @@ import torch
 
 from .errors import ConfigError, ShapeError
 from .kernels import CudaKernels, check_qkv, default_scale
-from .ring import NcclTransport, SoloTransport, ring_backward, ring_forward, run_ranks
+from .ring import (NcclTransport, SoloTransport, ring_backward, ring_backward_qtravel,
+                   ring_forward, run_ranks)
 from .schedule import shard, unshard
 from .trace import PassRecorder, PassTrace, merge
 
@@ -49,27 +50,29 @@ def _transport_for(group):
 
 class _BurstAttnFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, q, k, v, scale, causal, zigzag, transport, kernels, n_valid, recorders):
+    def forward(ctx, q, k, v, scale, causal, zigzag, transport, kernels, n_valid, recorders,
+                bwd_payload):
         rec_f, rec_b = recorders if recorders is not None else (None, None)
         o, lse = ring_forward(q, k, v, scale, causal, zigzag, transport, kernels, n_valid,
                               recorder=rec_f)
         ctx.save_for_backward(q, k, v, o, lse)
-        ctx.cfg = (scale, causal, zigzag, transport, kernels, n_valid, rec_b)
+        ctx.cfg = (scale, causal, zigzag, transport, kernels, n_valid, rec_b, bwd_payload)
         ctx.mark_non_differentiable(lse)
         return o, lse
 
     @staticmethod
     def backward(ctx, do, _dlse):
         q, k, v, o, lse = ctx.saved_tensors
-        scale, causal, zigzag, transport, kernels, n_valid, rec_b = ctx.cfg
-        dq, dk, dv = ring_backward(q, k, v, o, lse, do.contiguous(), scale, causal, zigzag,
-                                   transport, kernels, n_valid, recorder=rec_b)
-        return dq, dk, dv, None, None, None, None, None, None, None
+        scale, causal, zigzag, transport, kernels, n_valid, rec_b, bwd_payload = ctx.cfg
+        bwd = ring_backward_qtravel if bwd_payload == "q" else ring_backward
+        dq, dk, dv = bwd(q, k, v, o, lse, do.contiguous(), scale, causal, zigzag, transport,
+                         kernels, n_valid, recorder=rec_b)
+        return dq, dk, dv, None, None, None, None, None, None, None, None
 
 
 def burst_attn_func(q, k, v, causal: bool = False, softmax_scale: float | None = None,
                     group=None, zigzag: bool | None = None, valid_len: int | None = None, *,
-                    _transport=None, _kernels=None, _recorders=None):
+                    bwd_payload: str = "kv", _transport=None, _kernels=None, _recorders=None):
     """BurstAttention over the ranks of `group` (NCCL ring over NVLink).
 
     q, k, v: [batch, n_local, heads, head_dim] shards of the global sequence
@@ -79,6 +82,9 @@ def burst_attn_func(q, k, v, causal: bool = False, softmax_scale: float | None =
     `valid_len`: real global sequence length when the shards were zero-padded to
     a multiple of G (2G for zigzag); padded keys are excluded, padded rows of the
     outputs are meaningless (the reference's pad=True, ring.py:111-115).
+    `bwd_payload`: "kv" (default) rotates K/V and sends fp32 dK/dV contributions
+    home; "q" is the reference's payload (Q, dO, lse/D travel, K/V/dK/dV pinned,
+    ring.py:65-83) with fp32 dQ contributions sent home.
     `_recorders`: optional (forward, backward) trace.PassRecorder pair that
     records this rank's measured hop timeline and byte ledger.
     """
@@ -96,8 +102,10 @@ def burst_attn_func(q, k, v, causal: bool = False, softmax_scale: float | None =
         raise ShapeError("zigzag shards need an even local length")
     if valid_len is not None and not 0 < valid_len <= q.shape[1] * transport.world:
         raise ShapeError(f"valid_len={valid_len} outside (0, {q.shape[1] * transport.world}]")
+    if bwd_payload not in ("kv", "q"):
+        raise ConfigError(f"bwd_payload must be 'kv' or 'q', got {bwd_payload!r}")
     return _BurstAttnFn.apply(q, k, v, scale, bool(causal), bool(zigzag), transport, kernels,
-                              valid_len, _recorders)
+                              valid_len, _recorders, bwd_payload)
 
 
 @dataclass
@@ -113,7 +121,8 @@ class PassResult:
 
 def run_ring_pass(q, k, v, world: int, causal: bool = False, softmax_scale: float | None = None,
                   dout=None, zigzag: bool | None = None, kernels=None,
-                  pad: bool = False, trace: bool = False) -> PassResult:
+                  pad: bool = False, trace: bool = False,
+                  bwd_payload: str = "kv") -> PassResult:
     """Whole-ring forward (+ backward when `dout` is given) of GLOBAL tensors
     [batch, N, heads, head_dim] over `world` simulated devices on this GPU.
 
@@ -125,6 +134,8 @@ def run_ring_pass(q, k, v, world: int, causal: bool = False, softmax_scale: floa
     """
     if world < 1:
         raise ConfigError(f"gpus must be a positive integer, got {world}")
+    if bwd_payload not in ("kv", "q"):
+        raise ConfigError(f"bwd_payload must be 'kv' or 'q', got {bwd_payload!r}")
     kernels = kernels if kernels is not None else _default_kernels()
     if kernels.name == "cuda":
         check_qkv(q, k, v)
@@ -160,8 +171,9 @@ def run_ring_pass(q, k, v, world: int, causal: bool = False, softmax_scale: floa
                               recorder=rec_f[rank])
         if do_sh is None:
             return o, lse, None
-        g = ring_backward(qs, ks, vs, o, lse, do_sh[rank], scale, causal, zigzag, transport,
-                          kernels, n_valid, recorder=rec_b[rank])
+        bwd = ring_backward_qtravel if bwd_payload == "q" else ring_backward
+        g = bwd(qs, ks, vs, o, lse, do_sh[rank], scale, causal, zigzag, transport, kernels,
+                n_valid, recorder=rec_b[rank])
         return o, lse, g
 
     res = run_ranks(world, one)

@@ -130,6 +130,32 @@ __global__ void bwd_finalize_kernel(int B, int H, int D, int64_t n, const float*
   }
 }
 
+// out = sum of TL parts (gradient assembly from per-hop contributions)
+template <typename T>
+__global__ void tl_sum_kernel(int B, int H, int D, int64_t n, Parts parts, int nparts,
+                              T* __restrict__ out) {
+  const int64_t NT = ceil_div(n, 128);
+  const int64_t total = (int64_t)B * H * NT * (D / 4) * 128;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i & 127;
+    int64_t rest = i >> 7;
+    const int c4 = (int)(rest % (D / 4));
+    rest /= (D / 4);
+    const int64_t tile = rest % NT;
+    const int64_t bh = rest / NT;
+    const int64_t row = tile * 128 + r;
+    if (row >= n) continue;
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < nparts; ++k) {
+      const float4 a = *reinterpret_cast<const float4*>(parts.p[k] + i * 4);
+      s.x += a.x; s.y += a.y; s.z += a.z; s.w += a.w;
+    }
+    const int64_t b = bh / H, h = bh % H;
+    st4<T>(out + ((b * n + row) * H + h) * D + c4 * 4, s.x, s.y, s.z, s.w);
+  }
+}
+
 // Zero the rows of a TL contribution buffer outside [lo, hi): a hop's LAO-bwd
 // writes (accumulate = 0) only the visiting key rows it covers, so a partial
 // key range (K_EARLY_HALF, padded shards) leaves the rest to this kernel.

@@ -476,6 +476,27 @@ int burst_bwd_finalize(int dtype, int batch, int heads, int head_dim, int64_t n,
   return BURST_OK;
 }
 
+int burst_tl_sum(int dtype, int batch, int heads, int head_dim, int64_t n, const float* const* parts,
+                 int nparts, void* out, void* stream) {
+  int rc = check_dims(dtype, batch, heads, head_dim, n);
+  if (rc) return rc;
+  if (nparts < 1 || nparts > 16) return fail(BURST_E_SHAPE, "nparts must be in [1, 16]");
+  if (!out) return fail(BURST_E_SHAPE, "out must not be NULL");
+  if (n == 0) return BURST_OK;
+  aux::Parts pp;
+  for (int i = 0; i < 16; ++i) pp.p[i] = i < nparts ? parts[i] : nullptr;
+  const int64_t work = (int64_t)burst_workspace_floats(batch, heads, head_dim, n) / 4;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == BURST_DTYPE_BF16)
+    aux::tl_sum_kernel<__nv_bfloat16><<<grid_for(work, 256), 256, 0, st>>>(
+        batch, heads, head_dim, n, pp, nparts, (__nv_bfloat16*)out);
+  else
+    aux::tl_sum_kernel<float><<<grid_for(work, 256), 256, 0, st>>>(batch, heads, head_dim, n, pp,
+                                                                  nparts, (float*)out);
+  CHECK_LAUNCH();
+  return BURST_OK;
+}
+
 int burst_read_flags(void* stream, int* flags_out) {
   int* f = device_flags();
   if (!f) return fail(BURST_E_CUDA, "flag buffer allocation failed");

@@ -349,10 +349,11 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
 #pragma unroll
         for (int c4 = 0; c4 < 16; ++c4) {
           const float4 L = lse4[c4];
-          pr[4 * c4 + 0] = ptx::ex2(fmaf(__uint_as_float(r[4 * c4 + 0]), c2, -L.x));
-          pr[4 * c4 + 1] = ptx::ex2(fmaf(__uint_as_float(r[4 * c4 + 1]), c2, -L.y));
-          pr[4 * c4 + 2] = ptx::ex2(fmaf(__uint_as_float(r[4 * c4 + 2]), c2, -L.z));
-          pr[4 * c4 + 3] = ptx::ex2(fmaf(__uint_as_float(r[4 * c4 + 3]), c2, -L.w));
+          // masked entries are zeroed below, so the FMA-pipe exp2 is safe everywhere here
+          pr[4 * c4 + 0] = ptx::ex2_mixed(fmaf(__uint_as_float(r[4 * c4 + 0]), c2, -L.x), 4 * c4 + 0);
+          pr[4 * c4 + 1] = ptx::ex2_mixed(fmaf(__uint_as_float(r[4 * c4 + 1]), c2, -L.y), 4 * c4 + 1);
+          pr[4 * c4 + 2] = ptx::ex2_mixed(fmaf(__uint_as_float(r[4 * c4 + 2]), c2, -L.z), 4 * c4 + 2);
+          pr[4 * c4 + 3] = ptx::ex2_mixed(fmaf(__uint_as_float(r[4 * c4 + 3]), c2, -L.w), 4 * c4 + 3);
         }
       }
       if (!warp_full) {

@@ -238,7 +238,8 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
         for (int i = 0; i < BN; ++i) s[i] = __uint_as_float(r[i]);
       }
       const int64_t nvalid = lim - (int64_t)j * BN;
-      if (__any_sync(0xffffffffu, nvalid < BN)) {
+      const bool partial = __any_sync(0xffffffffu, nvalid < BN);
+      if (partial) {
 #pragma unroll
         for (int i = 0; i < BN; ++i)
           if (i >= nvalid) s[i] = -INFINITY;
@@ -272,13 +273,18 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
       }
       const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
       float ls8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      // part of the row's exp2 on the FMA pipe (ex2_poly) when no entry of the warp's
+      // tile is masked; masked (-inf) entries must stay exactly 0 -> MUFU only
+      const bool poly = !partial;
 #pragma unroll
       for (int cc = 0; cc < BN / 64; ++cc) {
         uint32_t pk[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          const float p0 = ptx::ex2(fmaf(s[cc * 64 + 2 * i], c2, -m_use));
-          const float p1 = ptx::ex2(fmaf(s[cc * 64 + 2 * i + 1], c2, -m_use));
+          const float x0 = fmaf(s[cc * 64 + 2 * i], c2, -m_use);
+          const float x1 = fmaf(s[cc * 64 + 2 * i + 1], c2, -m_use);
+          const float p0 = poly ? ptx::ex2_mixed(x0, i) : ptx::ex2(x0);
+          const float p1 = poly ? ptx::ex2_mixed(x1, i) : ptx::ex2(x1);
           ls8[(2 * i) & 7] += p0;
           ls8[(2 * i + 1) & 7] += p1;
           pk[i] = ptx::pack_bf16(p0, p1);

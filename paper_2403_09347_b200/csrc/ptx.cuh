@@ -355,6 +355,30 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 #endif
 }
+// 2^x on the FMA pipe (no MUFU): round-to-nearest split x = n + f, f in [-0.5, 0.5],
+// degree-3 polynomial for 2^f (max rel. error 7.7e-5, far below the bf16 rounding
+// of P), n added to the exponent field.  Offloads part of a softmax row from the
+// 16/clk/SM MUFU unit.  x is clamped below at -125 (result >= 2^-125, never 0:
+// callers use it only where masked entries are zeroed separately or absent).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -125.f);
+  const float j = x + 12582912.f;           // 1.5 * 2^23: integer part in the low mantissa
+  const float f = x - (j - 12582912.f);
+  float p = fmaf(0.05508868380751114f, f, 0.24260405145947936f);
+  p = fmaf(p, f, 0.6932762416819607f);
+  p = fmaf(p, f, 0.9999289403695112f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(j) << 23));
+}
+#ifndef BURST_POLY_MOD        // exp2 emulation share (default OFF: measured slower, the softmax
+                              // is issue-bound, profiles/r01_poly_exp2.txt): ex2_poly when
+#define BURST_POLY_MOD 4      // (idx % BURST_POLY_MOD) < BURST_POLY_CNT
+#endif
+#ifndef BURST_POLY_CNT
+#define BURST_POLY_CNT 0
+#endif
+__device__ __forceinline__ float ex2_mixed(float x, int idx) {
+  return (BURST_POLY_CNT > 0 && (idx % BURST_POLY_MOD) < BURST_POLY_CNT) ? ex2_poly(x) : ex2(x);
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);

@@ -158,6 +158,37 @@ class CudaKernels:
         _lib.call("burst_bwd_finalize", dtype_code(dq), B, H, D, n, _ptr(st.dq_acc), arr_k, arr_v,
                   np_, _ptr(dq), _ptr(dk), _ptr(dv), _stream_handle(stream))
 
+    # ------------------------------------------------ travelling-query backward (f2)
+    def stats_tensors(self, st: BwdState) -> list:
+        """The per-query-block backward statistics that travel with Q and dO."""
+        return [st.stats]
+
+    def visiting_state(self, st: BwdState, stats: list, dq_part) -> BwdState:
+        """Backward state of a visiting query block: its statistics, and the fresh
+        dQ contribution buffer this hop reduces into."""
+        return BwdState(stats[0], dq_part)
+
+    def dq_part(self, q: torch.Tensor, stream=None) -> torch.Tensor:
+        """A zeroed fp32 dQ contribution buffer (TL layout) for a visiting block."""
+        B, n, H, D = q.shape
+        buf = torch.empty(ws_floats(B, H, D, n), dtype=torch.float32, device=q.device)
+        with torch.cuda.stream(stream) if stream is not None else _nullctx():
+            buf.zero_()
+        return buf
+
+    def tl_sum(self, parts, out, stream=None) -> None:
+        B, n, H, D = out.shape
+        arr = (ctypes.c_void_p * len(parts))(*[p.data_ptr() for p in parts])
+        _lib.call("burst_tl_sum", dtype_code(out), B, H, D, n, arr, len(parts), _ptr(out),
+                  _stream_handle(stream))
+
+    def bwd_finalize_qtravel(self, st: BwdState, dq_parts, dk_acc, dv_acc, dq, dk, dv,
+                             stream=None) -> None:
+        """dq = own accumulator + received contributions; dk/dv = pinned accumulators."""
+        self.tl_sum([st.dq_acc] + list(dq_parts), dq, stream)
+        self.tl_sum([dk_acc], dk, stream)
+        self.tl_sum([dv_acc], dv, stream)
+
     def read_flags(self, stream=None) -> int:
         out = ctypes.c_int32(0)
         _lib.call("burst_read_flags", _stream_handle(stream), ctypes.byref(out))
@@ -167,3 +198,11 @@ class CudaKernels:
 def default_scale(head_dim: int) -> float:
     """softmax scale d^-0.5 (runner.py:154)."""
     return 1.0 / math.sqrt(head_dim)
+
+
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False

@@ -72,6 +72,18 @@ class _Streams:
         if self.cuda:
             self.comm.wait_stream(self.compute)
 
+    def compute_mark(self):
+        """Event at the compute stream's current tail (None on CPU)."""
+        if not self.cuda:
+            return None
+        ev = torch.cuda.Event()
+        ev.record(self.compute)
+        return ev
+
+    def comm_wait(self, ev):
+        if ev is not None:
+            self.comm.wait_event(ev)
+
     def compute_after_comm(self):
         if self.cuda:
             self.compute.wait_stream(self.comm)
@@ -253,13 +265,27 @@ def ring_forward(q, k, v, scale: float, causal: bool, zigzag: bool, transport, k
     cur_k, cur_v = k, v
     spare = None
     finalized = False
+    prev = S.compute_mark()      # compute tail before hop h (buffers it still reads)
     for h in range(G):
         plan = plan_hop(r, G, h, n, causal, zigzag, n_valid)
         exchanged = False
+        # launch the hop's kernel first, then post the transfer on the comm stream:
+        # both run concurrently (the comm waits only for the PREVIOUS hop's kernel,
+        # which last read the buffer being received into)
+        if recorder is not None:
+            recorder.mark(h, "compute_start", S.compute)
+        if not plan.skip:
+            fin = h == G - 1 and plan.covers_all_queries(n)
+            kernels.fwd(plan, q, cur_k, cur_v, scale, state, o, lse, first=(h == 0), finalize=fin,
+                        stream=S.compute)
+            finalized = finalized or fin
+        if recorder is not None:
+            recorder.mark(h, "compute_end", S.compute)
+        done = S.compute_mark()
         if h < G - 1:
             if spare is None:
                 spare = (torch.empty_like(k), torch.empty_like(v))
-            S.comm_after_compute()
+            S.comm_wait(prev)
             ops = [(SEND, cur_k, (r + 1) % G), (SEND, cur_v, (r + 1) % G),
                    (RECV, spare[0], (r - 1) % G), (RECV, spare[1], (r - 1) % G)]
             if recorder is not None:
@@ -270,15 +296,7 @@ def ring_forward(q, k, v, scale: float, causal: bool, zigzag: bool, transport, k
                 recorder.mark(h, "send_end", S.comm)
                 recorder.mark(h, "recv_ready", S.comm)
             exchanged = True
-        if recorder is not None:
-            recorder.mark(h, "compute_start", S.compute)
-        if not plan.skip:
-            fin = h == G - 1 and plan.covers_all_queries(n)
-            kernels.fwd(plan, q, cur_k, cur_v, scale, state, o, lse, first=(h == 0), finalize=fin,
-                        stream=S.compute)
-            finalized = finalized or fin
-        if recorder is not None:
-            recorder.mark(h, "compute_end", S.compute)
+        prev = done
         if exchanged:
             S.compute_after_comm()
             (cur_k, cur_v), spare = spare, (cur_k, cur_v)
@@ -318,8 +336,25 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
     received = []
     cur_k, cur_v = k, v
     spare = None
+    prev = S.compute_mark()
     for h in range(G):
         plan = plan_hop(r, G, h, n, causal, zigzag, n_valid)
+        # the hop's kernel first, then the transfers (which wait only for hop h-1's
+        # kernel: it produced the contribution sent now and last read `spare`)
+        if recorder is not None:
+            recorder.mark(h, "compute_start", S.compute)
+        if h == 0:
+            target = own
+        else:
+            if send[h % 2] is None:
+                send[h % 2] = (kernels.part(k), kernels.part(v))
+            target = send[h % 2]
+        if not plan.skip:
+            kernels.bwd(plan, q, cur_k, cur_v, dout, scale, st, target[0], target[1],
+                        accumulate=False, stream=S.compute)
+        if recorder is not None:
+            recorder.mark(h, "compute_end", S.compute)
+        done = S.compute_mark()
         ops = []
         if h < G - 1:
             if spare is None:
@@ -337,7 +372,7 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
         # transports in lockstep when causal hops are skipped
         slot = h < G - 1 or h >= 2
         if slot:
-            S.comm_after_compute()
+            S.comm_wait(prev)
             if recorder is not None:
                 recorder.count_send("backward", ops)
                 recorder.mark(h, "send_start", S.comm)
@@ -345,19 +380,7 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
             if recorder is not None:
                 recorder.mark(h, "send_end", S.comm)
                 recorder.mark(h, "recv_ready", S.comm)
-        if recorder is not None:
-            recorder.mark(h, "compute_start", S.compute)
-        if h == 0:
-            target = own
-        else:
-            if send[h % 2] is None:
-                send[h % 2] = (kernels.part(k), kernels.part(v))
-            target = send[h % 2]
-        if not plan.skip:
-            kernels.bwd(plan, q, cur_k, cur_v, dout, scale, st, target[0], target[1],
-                        accumulate=False, stream=S.compute)
-        if recorder is not None:
-            recorder.mark(h, "compute_end", S.compute)
+        prev = done
         if slot:
             S.compute_after_comm()
         if h < G - 1:
@@ -384,17 +407,150 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
     return dq, dk, dv
 
 
+def _qpart_exchange(r: int, G: int, n: int, causal: bool, zigzag: bool, hop: int, send_buf,
+                    kernels, like_q, n_valid=None):
+    """Ops moving the dQ contribution computed at `hop` (for the visiting query
+    block) to that block's home rank, and receiving the one computed for ours."""
+    ops, recv_buf = [], None
+    src = (r - hop) % G                        # origin of the query block I processed
+    if not plan_hop(src, G, (src - r) % G, n, causal, zigzag, n_valid).skip:
+        ops.append((SEND, send_buf, src))
+    c = (r + hop) % G                          # the rank that processed MY block at `hop`
+    if not plan_hop(r, G, (r - c) % G, n, causal, zigzag, n_valid).skip:
+        recv_buf = kernels.dq_part(like_q)
+        ops.append((RECV, recv_buf, c))
+    return ops, recv_buf
+
+
+def ring_backward_qtravel(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: bool,
+                          transport, kernels, n_valid: int | None = None, recorder=None):
+    """One rank's backward pass with the REFERENCE's payload:
+    the query-side record (Q, dO, lse/D statistics) travels the ring and K/V/dK/dV
+    stay pinned (BackwardBody ring.py:65-83, backward_step ring.py:221-242,
+    Alg. 2 of the paper).  The reference also carries the dQ accumulator in the
+    body; here each hop's dQ contribution goes home one hop later instead (the
+    lag sim.py:19-21 says a real system needs), so no transfer waits on a kernel
+    of the same hop.  Wire bytes per hop: 2·n·H·D·elem (Q, dO) + statistics
+    + an fp32 dQ contribution, vs K/V + fp32 dK/dV for ring_backward.
+    Returns (dq, dk, dv) in q's dtype."""
+    B, n, H, D = q.shape
+    G, r = transport.world, transport.rank
+    S = _Streams(q.device)
+    st = kernels.bwd_prepare(o, dout, lse, stream=S.compute)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    dk_acc, dv_acc = kernels.part(k), kernels.part(v)
+    payload = [q, dout] + kernels.stats_tensors(st)      # the visiting query block
+    spare = None
+    send = [None, None]
+    received = []
+    first_kv = True
+    prev = S.compute_mark()
+    for h in range(G):
+        src = (r - h) % G
+        plan = plan_hop(src, G, (src - r) % G, n, causal, zigzag, n_valid)
+        if recorder is not None:
+            recorder.mark(h, "compute_start", S.compute)
+        if h == 0:
+            vst = st                                     # own queries: own dQ accumulator
+        else:
+            send[h % 2] = kernels.dq_part(q, stream=S.compute)
+            vst = kernels.visiting_state(st, payload[2:], send[h % 2])
+        if not plan.skip:
+            kernels.bwd(plan, payload[0], k, v, payload[1], scale, vst, dk_acc, dv_acc,
+                        accumulate=not first_kv, stream=S.compute)
+            first_kv = False
+        if recorder is not None:
+            recorder.mark(h, "compute_end", S.compute)
+        done = S.compute_mark()
+        ops = []
+        if h < G - 1:
+            if spare is None:
+                spare = [torch.empty_like(t) for t in payload]
+            ops += [(SEND, t, (r + 1) % G) for t in payload]
+            ops += [(RECV, t, (r - 1) % G) for t in spare]
+        if h >= 2:
+            p_ops, got = _qpart_exchange(r, G, n, causal, zigzag, h - 1, send[(h - 1) % 2],
+                                         kernels, q, n_valid)
+            ops += p_ops
+            if got is not None:
+                received.append(got)
+        slot = h < G - 1 or h >= 2
+        if slot:
+            S.comm_wait(prev)
+            if recorder is not None:
+                recorder.count_send("backward", ops)
+                recorder.mark(h, "send_start", S.comm)
+            transport.sendrecv(ops, S.comm)
+            if recorder is not None:
+                recorder.mark(h, "send_end", S.comm)
+                recorder.mark(h, "recv_ready", S.comm)
+        prev = done
+        if slot:
+            S.compute_after_comm()
+        if h < G - 1:
+            payload, spare = spare, payload
+            if spare[0] is q:
+                spare = None   # never receive into the caller's tensors
+    if first_kv:                                  # every hop skipped: no key is visible
+        for t in (dk_acc, dv_acc):
+            t.zero_()
+    if G > 1:
+        p_ops, got = _qpart_exchange(r, G, n, causal, zigzag, G - 1, send[(G - 1) % 2], kernels,
+                                     q, n_valid)
+        if got is not None:
+            received.append(got)
+        S.comm_after_compute()
+        if recorder is not None:
+            recorder.count_send("backward", p_ops)
+            recorder.mark(G, "send_start", S.comm)
+        transport.sendrecv(p_ops, S.comm)
+        if recorder is not None:
+            recorder.mark(G, "send_end", S.comm)
+            recorder.mark(G, "recv_ready", S.comm)
+        S.compute_after_comm()
+    kernels.bwd_finalize_qtravel(st, received, dk_acc, dv_acc, dq, dk, dv, stream=S.compute)
+    return dq, dk, dv
+
+
 def ring_comm_bytes(n_local: int, batch: int, heads: int, d: int, world: int, elem: int,
-                    causal: bool, zigzag: bool, rank: int = 0) -> tuple[int, int]:
+                    causal: bool, zigzag: bool, rank: int = 0,
+                    bwd_payload: str = "kv") -> tuple[int, int]:
     """Bytes `rank` sends per forward and per backward pass (the ledger of
-    sim.py:118-153, for the K/V + fp32 dK/dV payload of this build)."""
+    sim.py:118-153).  bwd_payload "kv": K/V + fp32 dK/dV contributions (this
+    build's default); "q": Q, dO, lse/D statistics + fp32 dQ contributions (the
+    reference's payload, ring_backward_qtravel)."""
     kv = 2 * batch * n_local * heads * d * elem
-    part = 2 * batch * (-(-n_local // 128) * 128) * heads * d * 4
+    nt = -(-n_local // 128) * 128
     fwd = (world - 1) * kv
+    if bwd_payload == "q":
+        stats = 2 * batch * heads * nt * 4
+        qpart = batch * nt * heads * d * 4
+        bwd = (world - 1) * (kv + stats)
+        for h in range(1, world):
+            src = (rank - h) % world
+            if not plan_hop(src, world, (src - rank) % world, n_local, causal, zigzag).skip:
+                bwd += qpart
+        return fwd, bwd
+    part = 2 * batch * nt * heads * d * 4
     bwd = (world - 1) * kv
     bwd += sum(part for h in range(1, world)
                if not plan_hop(rank, world, h, n_local, causal, zigzag).skip)
     return fwd, bwd
+
+
+_loopback_streams: dict = {}   # (device, rank) -> (compute stream, {device: comm stream})
+_loopback_lock = threading.Lock()
+
+
+def _rank_streams(dev: int, rank: int):
+    """Persistent streams of a loopback rank: repeated passes reuse the same
+    streams (and so the caching allocator's per-stream pools)."""
+    with _loopback_lock:
+        key = (dev, rank)
+        if key not in _loopback_streams:
+            _loopback_streams[key] = (torch.cuda.Stream(device=dev),
+                                      {dev: torch.cuda.Stream(device=dev, priority=-1)})
+        return _loopback_streams[key]
 
 
 def run_ranks(world: int, fn, timeout: float = 600.0) -> Sequence:
@@ -409,7 +565,8 @@ def run_ranks(world: int, fn, timeout: float = 600.0) -> Sequence:
         try:
             if dev is not None:
                 torch.cuda.set_device(dev)
-                s = torch.cuda.Stream()
+                s, comm = _rank_streams(dev, rank)
+                _tls.streams = comm
                 with torch.cuda.stream(s):
                     out[rank] = fn(rank, hub.transport(rank))
                 s.synchronize()

@@ -98,3 +98,21 @@ class OracleKernels:
         dq.copy_(torch.from_numpy(st["dq"]).to(dq.dtype))
         dk.copy_(sum(p for p in dk_parts).to(dk.dtype))
         dv.copy_(sum(p for p in dv_parts).to(dv.dtype))
+
+    # travelling-query backward (f2)
+    def stats_tensors(self, st):
+        return [torch.from_numpy(st["lse"].copy()), torch.from_numpy(st["D"].copy())]
+
+    def visiting_state(self, st, stats, dq_part):
+        return {"lse": stats[0].numpy(), "D": stats[1].numpy(), "dq": dq_part.numpy()}
+
+    def dq_part(self, q, stream=None):
+        return torch.zeros(tuple(q.shape), dtype=torch.float64)
+
+    def bwd_finalize_qtravel(self, st, dq_parts, dk_acc, dv_acc, dq, dk, dv, stream=None):
+        self.launches += 1
+        tot = torch.from_numpy(st["dq"]) + sum((p for p in dq_parts), torch.zeros(tuple(dq.shape),
+                                                                                  dtype=torch.float64))
+        dq.copy_(tot.to(dq.dtype))
+        dk.copy_(dk_acc.to(dk.dtype))
+        dv.copy_(dv_acc.to(dv.dtype))

@@ -99,6 +99,32 @@ def test_bf16_zigzag_unaligned_chunks(N, world):
         assert max_abs(got, ref) < BF16_TOL
 
 
+@pytest.mark.parametrize("world,causal,zigzag", [(2, False, False), (4, True, True),
+                                                 (4, True, False)])
+def test_ring_bf16_reference_payload(world, causal, zigzag):
+    """bwd_payload="q" (the reference's Q/dO/lse/D payload, K/V/dK/dV pinned)."""
+    from paper_2403_09347_b200 import run_ring_pass
+    N = 256 * world * (2 if zigzag else 1)
+    q, k, v, do = make_inputs(1, N, 2, 128, seed=20 + world)
+    poison_allocator()
+    res = run_ring_pass(q, k, v, world, causal=causal, dout=do, zigzag=zigzag, bwd_payload="q")
+    torch.cuda.synchronize()
+    o, lse, dq, dk, dv = oracle_ring(q, k, v, do, world, causal, zigzag)
+    for got, ref in ((res.out, o), (res.dq, dq), (res.dk, dk), (res.dv, dv)):
+        assert max_abs(got, ref) < BF16_TOL
+
+
+def test_f32_reference_payload_rel_1e5():
+    from paper_2403_09347_b200 import run_ring_pass
+    q, k, v, do = make_inputs(1, 416, 2, 32, seed=12, dtype=torch.float32)
+    poison_allocator()
+    res = run_ring_pass(q, k, v, 2, causal=True, dout=do, zigzag=True, bwd_payload="q")
+    torch.cuda.synchronize()
+    o, lse, dq, dk, dv = oracle_ring(q, k, v, do, 2, True, True)
+    for got, ref in ((res.dq, dq), (res.dk, dk), (res.dv, dv)):
+        assert rel_err(got, ref) < 1e-5
+
+
 def test_c1_golden_fp32(golden):
     """BASELINE configs[0] (seq 1024, d 64, 2 heads, G 2, fp32) against the
     reference's own outputs (tests/golden, produced by the reference)."""

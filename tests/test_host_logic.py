@@ -158,7 +158,7 @@ def test_engine_loopback_matches_dense(G, causal, zigzag):
     _check(res, q, k, v, do, causal)
 
 
-def _gloo_worker(rank, world, port, causal, zigzag, out_dir):
+def _gloo_worker(rank, world, port, causal, zigzag, out_dir, bwd_payload="kv"):
     import torch.distributed as dist
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -174,15 +174,17 @@ def _gloo_worker(rank, world, port, causal, zigzag, out_dir):
     q, k, v, do = (torch.randn(1, N, 2, 8, generator=g, dtype=torch.float64) for _ in range(4))
     sh = [shard(t, rank, world, zigzag).requires_grad_(i < 3) for i, t in enumerate((q, k, v, do))]
     o, lse = burst_attn_func(sh[0], sh[1], sh[2], causal=causal, zigzag=zigzag,
-                             _transport=TorchDistTransport(), _kernels=OK())
+                             bwd_payload=bwd_payload, _transport=TorchDistTransport(),
+                             _kernels=OK())
     o.backward(sh[3])
     torch.save({"o": o.detach(), "lse": lse, "dq": sh[0].grad, "dk": sh[1].grad,
                 "dv": sh[2].grad}, os.path.join(out_dir, f"r{rank}.pt"))
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("causal,zigzag", [(False, False), (True, True), (True, False)])
-def test_engine_gloo_two_processes(causal, zigzag, tmp_path):
+@pytest.mark.parametrize("causal,zigzag,payload", [(False, False, "kv"), (True, True, "kv"),
+                                                   (True, False, "kv"), (True, True, "q")])
+def test_engine_gloo_two_processes(causal, zigzag, payload, tmp_path):
     import socket
     import torch.multiprocessing as mp
     from paper_2403_09347_b200.schedule import unshard
@@ -191,7 +193,7 @@ def test_engine_gloo_two_processes(causal, zigzag, tmp_path):
     port = s.getsockname()[1]
     s.close()
     world = 2
-    mp.start_processes(_gloo_worker, args=(world, port, causal, zigzag, str(tmp_path)),
+    mp.start_processes(_gloo_worker, args=(world, port, causal, zigzag, str(tmp_path), payload),
                        nprocs=world, start_method="spawn", join=True)
     parts = [torch.load(tmp_path / f"r{r}.pt") for r in range(world)]
 
@@ -249,3 +251,53 @@ def test_valid_rows_is_prefix():
                 want = [p < nv for p in pos]
                 k = valid_rows(r, G, n, zz, nv)
                 assert want == [True] * k + [False] * (n - k)
+
+
+# ---------------------------------------------------------------- reference payload (f2)
+
+@pytest.mark.parametrize("G,causal,zigzag", [(1, False, False), (2, False, False),
+                                             (3, False, False), (4, True, False),
+                                             (4, True, True), (3, True, True)])
+def test_qtravel_payload_matches_dense(G, causal, zigzag):
+    """bwd_payload="q": Q/dO/lse/D travel, K/V/dK/dV pinned (ring.py:65-83, 221-242)."""
+    from paper_2403_09347_b200 import run_ring_pass
+    g = torch.Generator().manual_seed(10 + G)
+    N = 16 * G
+    q, k, v, do = (torch.randn(2, N, 2, 8, generator=g, dtype=torch.float64) for _ in range(4))
+    res = run_ring_pass(q, k, v, G, causal=causal, dout=do, zigzag=zigzag,
+                        kernels=OracleKernels(), bwd_payload="q")
+    _check(res, q, k, v, do, causal)
+
+
+@pytest.mark.parametrize("name,zigzag", [("ring_n100_d16_h2_g3_pad_f32", False),
+                                         ("ring_n98_d16_h1_g4_causal_pad_f32", True)])
+def test_qtravel_padding_matches_reference_golden(golden, name, zigzag):
+    from paper_2403_09347_b200 import run_ring_pass
+    g = golden(name)
+    seq, dim, heads, gpus, seed, causal, tile, prec = (int(x) for x in g["meta"])
+    q, k, v, do, scale = orc.generate_inputs(seq, dim, heads, 1, seed, np.float64)
+    to = lambda a: torch.from_numpy(np.ascontiguousarray(a.transpose(1, 0, 2)[None]))
+    res = run_ring_pass(to(q), to(k), to(v), gpus, causal=bool(causal), dout=to(do),
+                        zigzag=zigzag, kernels=OracleKernels(), pad=True, bwd_payload="q")
+    for key, got in (("o", res.out), ("dq", res.dq), ("dk", res.dk), ("dv", res.dv)):
+        ref = g[key].transpose(1, 0, 2)[None]
+        assert np.max(np.abs(got.numpy() - ref)) / np.max(np.abs(ref)) < 1e-5, key
+
+
+@pytest.mark.parametrize("causal,zigzag", [(False, False), (True, True)])
+def test_qtravel_ledger_counts_fewer_elements(causal, zigzag):
+    """The reference payload moves Q + dO (+ lse, D) instead of K + V and fp32 dK + dV:
+    ledger element counts from the measured run equal ring_comm_bytes' model."""
+    from paper_2403_09347_b200 import run_ring_pass
+    G, N, H, D = 4, 64, 2, 8
+    g = torch.Generator().manual_seed(3)
+    q, k, v, do = (torch.randn(1, N, H, D, generator=g, dtype=torch.float64) for _ in range(4))
+    rq = run_ring_pass(q, k, v, G, causal=causal, dout=do, zigzag=zigzag,
+                       kernels=OracleKernels(), bwd_payload="q", trace=True)
+    n = N // G
+    for r, led in enumerate(rq.trace.ledgers):
+        from paper_2403_09347_b200.schedule import plan_hop
+        parts = sum(1 for h in range(1, G)
+                    if not plan_hop((r - h) % G, G, (-h) % G, n, causal, zigzag).skip)
+        # Q, dO (n*H*D each), lse + D (H*n each) per rotation; one dQ part per visited block
+        assert led.elements_sent_backward == (G - 1) * (2 * n * H * D + 2 * H * n) + parts * n * H * D

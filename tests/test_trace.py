@@ -90,10 +90,10 @@ def test_gpu_ring_trace_hides_comm():
     > 0: the fraction is printed for the record)."""
     from paper_2403_09347_b200 import run_ring_pass
     from paper_2403_09347_b200.ring import ring_comm_bytes
-    G, N, H, D = 4, 16384, 8, 128
+    G, N, H, D = 4, 65536, 16, 128      # hops of several ms: the host runs ahead of the GPU
     g = torch.Generator().manual_seed(0)
     q, k, v, do = (torch.randn(1, N, H, D, generator=g).to(torch.bfloat16).cuda() for _ in range(4))
-    run_ring_pass(q, k, v, G, dout=do)        # warm-up
+    run_ring_pass(q, k, v, G, dout=do, trace=True)        # warm-up (streams, allocator pools)
     res = run_ring_pass(q, k, v, G, dout=do, trace=True)
     fwd_b, bwd_b = ring_comm_bytes(N // G, 1, H, D, G, 2, False, False)
     for led in res.trace.ledgers:
