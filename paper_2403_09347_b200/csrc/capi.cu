@@ -15,6 +15,7 @@
 #include "lao_bwd2_sm100.cuh"
 #include "lao_bwd3_sm100.cuh"
 #include "lao_bwd4_sm100.cuh"
+#include "lao_bwd5_sm100.cuh"
 #include "lao_bwd_sm100.cuh"
 #include "lao_fwd_sm100.cuh"
 #include "simt_f32.cuh"
@@ -70,6 +71,24 @@ int make_tmap(CUtensorMap* tm, const void* base, int64_t n, int H, int D, int B,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(BURST_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return BURST_OK;
+}
+
+// f32 TL workspace [B*H][NT][D/4][128][4] viewed as a 3-D tensor [G][128][4]
+// (G = B*H*NT*D/4 column groups) for TMA tensor reductions of 8-group x 64-row boxes.
+int make_tmap_tl(CUtensorMap* tm, const float* base, int64_t n, int H, int D, int B) {
+  auto fn = encode_fn();
+  if (!fn) return fail(BURST_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const int64_t G = (int64_t)B * H * ceil_div(n, 128) * (D / 4);
+  if (G > INT32_MAX) return fail(BURST_E_SHAPE, "workspace too large for TMA coordinates");
+  cuuint64_t dims[3] = {4, 128, (cuuint64_t)G};
+  cuuint64_t strides[2] = {16, 2048};
+  cuuint32_t box[3] = {4, 64, 8};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(BURST_E_CUDA, "cuTensorMapEncodeTiled (TL) failed: " + std::to_string((int)r));
   return BURST_OK;
 }
 
@@ -230,13 +249,45 @@ int launch_bwd2_bf16(const burst_hop* h, const void* q, const void* k, const voi
   return BURST_OK;
 }
 
+// CTA-pair backward with two P/dS warpgroups and SMEM-staged dQ reduction (variant 5).
+int launch_bwd5_bf16(const burst_hop* h, const void* q, const void* k, const void* v, const void* dout,
+                     const float* stats, float* dq_acc, float* dk, float* dv, int acc, cudaStream_t st) {
+  bwd5::Params p;
+  memset(&p, 0, sizeof(p));
+  int rc;
+  if ((rc = make_tmap(&p.tm_q128, q, h->n_q, h->heads, 128, h->batch))) return rc;
+  if ((rc = make_tmap(&p.tm_q64, q, h->n_q, h->heads, 128, h->batch, 64))) return rc;
+  if ((rc = make_tmap(&p.tm_do128, dout, h->n_q, h->heads, 128, h->batch))) return rc;
+  if ((rc = make_tmap(&p.tm_do64, dout, h->n_q, h->heads, 128, h->batch, 64))) return rc;
+  if ((rc = make_tmap(&p.tm_k, k, h->n_k, h->heads, 128, h->batch))) return rc;
+  if ((rc = make_tmap(&p.tm_v, v, h->n_k, h->heads, 128, h->batch))) return rc;
+  if ((rc = make_tmap_tl(&p.tm_dq, dq_acc, h->n_q, h->heads, 128, h->batch))) return rc;
+  p.stats = stats; p.dq_acc = dq_acc; p.dk_acc = dk; p.dv_acc = dv;
+  p.hop = *h;
+  p.scale_log2 = h->softmax_scale * kLog2e;
+  p.scale = h->softmax_scale;
+  p.accumulate = acc;
+#ifdef BURST_TRACE
+  p.trace = trace_buffer();
+#endif
+  static std::once_flag once;
+  static int attr_rc = 0;
+  std::call_once(once, [] { attr_rc = set_smem(bwd5::lao_bwd5_kernel, bwd5::kSmemBytes); });
+  if (attr_rc) return attr_rc;
+  dim3 grid((unsigned)(2 * ceil_div(h->k_len, 2 * bwd5::BN)), h->heads, h->batch);
+  bwd5::lao_bwd5_kernel<<<grid, bwd5::kThreads, bwd5::kSmemBytes, st>>>(p);
+  CHECK_LAUNCH();
+  return BURST_OK;
+}
+
 // Backward kernel variant for bf16 (BURST_BWD_KERNEL: 1 = single CTA + red.global,
 // 2 = CTA pair, 3 = single CTA + SMEM-staged TMA bulk reductions, 4 = variant 3 with two
-// P/dS warpgroups and a double-buffered dQ drain; default 4).
+// P/dS warpgroups and a double-buffered dQ drain, 5 = CTA pair with two P/dS warpgroups,
+// dS^T in TMEM and SMEM-staged dQ reduction; default 4).
 int bwd_variant() {
   static int v = [] {
     const char* e = getenv("BURST_BWD_KERNEL");
-    return (e && e[0] >= '1' && e[0] <= '4') ? e[0] - '0' : 4;
+    return (e && e[0] >= '1' && e[0] <= '5') ? e[0] - '0' : 4;
   }();
   return v;
 }
@@ -437,10 +488,11 @@ int burst_lao_bwd(const burst_hop* hop, const void* q, const void* k, const void
       if (var == 2) return launch_bwd2_bf16(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
       if (var == 3) return launch_bwd3_bf16<128>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
       if (var == 4) return launch_bwd4_bf16<128>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
+      if (var == 5) return launch_bwd5_bf16(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
       return launch_bwd_bf16<128>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
     }
     if (var == 3) return launch_bwd3_bf16<64>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
-    if (var == 4) return launch_bwd4_bf16<64>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
+    if (var >= 4) return launch_bwd4_bf16<64>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
     return launch_bwd_bf16<64>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
   }
   switch (hop->head_dim) {

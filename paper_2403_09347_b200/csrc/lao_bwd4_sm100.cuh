@@ -227,48 +227,58 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
     // ------------------------------------------------------------ MMA issuer
     // Per query tile i: dV_i | {S^T_{i+1}, dK_i + dQ_i -> dP region} in whichever
     // order their inputs arrive (S^T first when both are ready) | dP^T_{i+1} once
-    // dQ_i has been drained to registers.
-    if (lane == 0 && nq > 0) {
+    // dQ_i has been drained to registers.  The whole warp runs the loop (uniform
+    // control flow keeps descriptors in uniform registers); one elected lane issues
+    // each MMA group and its commits.  Descriptors: base + (byte offset >> 4).
+    if (nq > 0) {
       constexpr uint32_t id_kk = ptx::make_idesc_bf16(BN, BM, 0, 0);   // S^T, dP^T
       constexpr uint32_t id_kmn = ptx::make_idesc_bf16(BN, D, 0, 1);   // dV, dK (B MN-major)
       constexpr uint32_t id_mnmn = ptx::make_idesc_bf16(BM, D, 1, 1);  // dQ (A, B MN-major)
-      const uint32_t aK = ptx::smem_u32(sK), aV = ptx::smem_u32(sV);
-      const uint32_t aQ = ptx::smem_u32(sQ), adO = ptx::smem_u32(sdO), adS = ptx::smem_u32(sdS);
+      const uint64_t dK = ptx::make_sdesc(ptx::smem_u32(sK), 0, 1024);
+      const uint64_t dV = ptx::make_sdesc(ptx::smem_u32(sV), 0, 1024);
+      const uint64_t dQ0 = ptx::make_sdesc(ptx::smem_u32(sQ), 0, 1024);
+      const uint64_t dOk = ptx::make_sdesc(ptx::smem_u32(sdO), 0, 1024);           // K-major (dP^T)
+      const uint64_t dOm = ptx::make_sdesc(ptx::smem_u32(sdO), C::kBoxBytes, 1024); // MN-major (dV)
+      const uint64_t dQm0 = ptx::make_sdesc(ptx::smem_u32(sQ), C::kBoxBytes, 1024); // MN-major (dK)
+      const uint64_t dSk = ptx::make_sdesc(ptx::smem_u32(sdS), 0, 1024);           // dS^T K-major (dK)
+      const uint64_t dSm = ptx::make_sdesc(ptx::smem_u32(sdS), 16384, 1024);       // dS MN-major (dQ)
+      const uint64_t dKm = ptx::make_sdesc(ptx::smem_u32(sK), C::kBoxBytes, 1024);  // K MN-major (dQ)
+      constexpr uint64_t kStage = (uint64_t)(C::kTileBytes >> 4);
+      auto kmaj = [](int kk) -> uint64_t { return (uint64_t)(((kk >> 2) * C::kBoxBytes + (kk & 3) * 32) >> 4); };
       auto st_mma = [&](int stage) {   // S^T = K Q^T
-        const uint32_t q = aQ + stage * C::kTileBytes;
+        if (ptx::elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * C::kBoxBytes + (kk & 3) * 32;
-          ptx::mma_ss(tbase + kS, ptx::make_sdesc(aK + off, 0, 1024),
-                      ptx::make_sdesc(q + off, 0, 1024), id_kk, kk > 0);
+          for (int kk = 0; kk < D / 16; ++kk)
+            ptx::mma_ss(tbase + kS, dK + kmaj(kk), dQ0 + stage * kStage + kmaj(kk), id_kk, kk > 0);
+          ptx::mma_commit(s_full);
         }
-        ptx::mma_commit(s_full);
+        __syncwarp();
       };
       auto dpt_mma = [&]() {  // dP^T = V dO^T
+        if (ptx::elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * C::kBoxBytes + (kk & 3) * 32;
-          ptx::mma_ss(tbase + kDP, ptx::make_sdesc(aV + off, 0, 1024),
-                      ptx::make_sdesc(adO + off, 0, 1024), id_kk, kk > 0);
+          for (int kk = 0; kk < D / 16; ++kk)
+            ptx::mma_ss(tbase + kDP, dV + kmaj(kk), dOk + kmaj(kk), id_kk, kk > 0);
+          ptx::mma_commit(dp_full);
         }
-        ptx::mma_commit(dp_full);
+        __syncwarp();
       };
       auto dkq_mma = [&](int i) {   // dK += dS^T Q ; dQ_i = dS K (into the drained dP^T columns)
-        const uint32_t q = aQ + (i & 1) * C::kTileBytes;
+        if (ptx::elect_one()) {
+          const uint64_t qm = dQm0 + (i & 1) * kStage;
 #pragma unroll
-        for (int kk = 0; kk < BM / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-          ptx::mma_ss(tbase + kDK, ptx::make_sdesc(adS + off, 0, 1024),
-                      ptx::make_sdesc(q + kk * 2048, C::kBoxBytes, 1024), id_kmn,
-                      (i > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < BM / 16; ++kk)
+            ptx::mma_ss(tbase + kDK, dSk + (uint64_t)(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4),
+                        qm + (uint64_t)(kk * 2048 >> 4), id_kmn, (i > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+          for (int kk = 0; kk < BN / 16; ++kk)
+            ptx::mma_ss(tbase + kDP, dSm + (uint64_t)(kk * 2048 >> 4), dKm + (uint64_t)(kk * 2048 >> 4),
+                        id_mnmn, kk > 0);
+          ptx::mma_commit(dq_full);
+          ptx::mma_commit(ds_empty);
+          ptx::mma_commit(qdo_empty + (i & 1));
         }
-#pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk)
-          ptx::mma_ss(tbase + kDP, ptx::make_sdesc(adS + kk * 2048, 16384, 1024),
-                      ptx::make_sdesc(aK + kk * 2048, C::kBoxBytes, 1024), id_mnmn, kk > 0);
-        ptx::mma_commit(dq_full);
-        ptx::mma_commit(ds_empty);
-        ptx::mma_commit(qdo_empty + (i & 1));
+        __syncwarp();
       };
       ptx::mbar_wait(kv_full, 0);
       ptx::mbar_wait(qdo_full + 0, 0);
@@ -283,12 +293,14 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
         // dV += P^T dO   (A = P^T from TMEM: query half h at S^T columns [64h, 64h+32))
         ptx::mbar_wait(p_full, i & 1); BTRACE4(0, i);
         ptx::tc_fence_after();
+        if (ptx::elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < BM / 16; ++kk)
-          ptx::mma_ts(tbase + kDV, tbase + kS + (kk < 4 ? kk * 8 : 32 + kk * 8),
-                      ptx::make_sdesc(adO + kk * 2048, C::kBoxBytes, 1024), id_kmn,
-                      (i > 0 || kk > 0) ? 1u : 0u);
-        ptx::mma_commit(do_empty);
+          for (int kk = 0; kk < BM / 16; ++kk)
+            ptx::mma_ts(tbase + kDV, tbase + kS + (kk < 4 ? kk * 8 : 32 + kk * 8),
+                        dOm + (uint64_t)(kk * 2048 >> 4), id_kmn, (i > 0 || kk > 0) ? 1u : 0u);
+          ptx::mma_commit(do_empty);
+        }
+        __syncwarp();
         bool st_done = !more, dkq_done = false;
         while (!st_done || !dkq_done) {
           if (!st_done && ptx::mbar_try_wait(qdo_full + (s ^ 1), ((i + 1) >> 1) & 1)) {
@@ -311,7 +323,8 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
           dpt_mma();
         }
       }
-      ptx::mma_commit(dkv_full);
+      if (ptx::elect_one()) ptx::mma_commit(dkv_full);
+      __syncwarp();
     }
    }
   } else if (warp < 8) {

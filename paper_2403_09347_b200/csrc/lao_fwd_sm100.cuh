@@ -144,38 +144,47 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
     }
   } else if (warp == 9) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0 && nkv > 0) {
+    // Whole warp runs the loop (uniform control flow keeps descriptors in uniform
+    // registers); one elected lane issues each MMA group and its commits.
+    if (nkv > 0) {
       constexpr uint32_t idesc_qk = ptx::make_idesc_bf16(BM, BN, 0, 0);
       constexpr uint32_t idesc_pv = ptx::make_idesc_bf16(BM, D, 0, 1);
-      const uint32_t sQa = ptx::smem_u32(sQ);
-      const uint32_t sKVa = ptx::smem_u32(sKV);
+      const uint64_t dQk = ptx::make_sdesc(ptx::smem_u32(sQ), 0, 1024);
+      const uint64_t dKVk = ptx::make_sdesc(ptx::smem_u32(sKV), 0, 1024);            // K (K-major)
+      const uint64_t dKVm = ptx::make_sdesc(ptx::smem_u32(sKV), C::kBoxBytes, 1024); // V (MN-major)
+      constexpr uint64_t kTile = (uint64_t)(C::kTileBytes >> 4);
       auto qk = [&](int t, int slot) {
-        const uint32_t qa = sQa + t * C::kTileBytes;
-        const uint32_t ka = sKVa + slot * C::kTileBytes;
+        if (ptx::elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * C::kBoxBytes + (kk & 3) * 32;
-          ptx::mma_ss(tbase + t * 128, ptx::make_sdesc(qa + off, 0, 1024),
-                      ptx::make_sdesc(ka + off, 0, 1024), idesc_qk, kk > 0);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint64_t off = (uint64_t)(((kk >> 2) * C::kBoxBytes + (kk & 3) * 32) >> 4);
+            ptx::mma_ss(tbase + t * 128, dQk + t * kTile + off, dKVk + slot * kTile + off, idesc_qk,
+                        kk > 0);
+          }
+          ptx::mma_commit(s_full + t);
         }
+        __syncwarp();
       };
       auto pv = [&](int t, int slot, bool acc) {
-        const uint32_t va = sKVa + slot * C::kTileBytes;
+        if (ptx::elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk) {
-          ptx::mma_ts(tbase + 256 + t * D, tbase + t * 128 + kk * 8,
-                      ptx::make_sdesc(va + kk * 2048, C::kBoxBytes, 1024), idesc_pv,
-                      (acc || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < BN / 16; ++kk)
+            ptx::mma_ts(tbase + 256 + t * D, tbase + t * 128 + kk * 8,
+                        dKVm + slot * kTile + (uint64_t)(kk * 2048 >> 4), idesc_pv,
+                        (acc || kk > 0) ? 1u : 0u);
         }
+        __syncwarp();
+      };
+      auto commit = [&](uint64_t* b) {
+        if (ptx::elect_one()) ptx::mma_commit(b);
+        __syncwarp();
       };
       ptx::mbar_wait(q_full, 0);
       ptx::mbar_wait(kv_full + 0, 0);
       ptx::tc_fence_after();
       qk(0, 0);
-      ptx::mma_commit(s_full + 0);
       qk(1, 0);
-      ptx::mma_commit(s_full + 1);
-      ptx::mma_commit(kv_empty + 0);
+      commit(kv_empty + 0);
       for (int j = 0; j < nkv; ++j) {
         const int itv = 2 * j + 1, sv = itv % C::kStages;
         const int itk = 2 * j + 2, sk = itk % C::kStages;
@@ -188,19 +197,17 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
           ptx::mbar_wait(kv_full + sk, (itk / C::kStages) & 1);
           ptx::tc_fence_after();
           qk(0, sk);
-          ptx::mma_commit(s_full + 0);
         }
         ptx::mbar_wait(p_full + 1, j & 1);
         ptx::tc_fence_after();
         pv(1, sv, j > 0);
-        ptx::mma_commit(kv_empty + sv);
+        commit(kv_empty + sv);
         if (more) {
           qk(1, sk);
-          ptx::mma_commit(s_full + 1);
-          ptx::mma_commit(kv_empty + sk);
+          commit(kv_empty + sk);
         }
       }
-      ptx::mma_commit(o_full);
+      commit(o_full);
     }
    }
   } else {

@@ -321,6 +321,15 @@ __device__ __forceinline__ void bulk_reduce_add_f32(float* gdst, const void* ssr
                "r"(smem_u32(ssrc)), "r"(bytes)
                : "memory");
 }
+// TMA tensor reduction (add) of a 3-D box from SMEM into global (bulk-group completion)
+__device__ __forceinline__ void tma_reduce_add_3d(const void* tmap, const void* ssrc, int c0, int c1,
+                                                  int c2) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+          reinterpret_cast<uint64_t>(tmap)),
+      "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(ssrc))
+      : "memory");
+}
 __device__ __forceinline__ void bulk_commit() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
