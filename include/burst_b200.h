@@ -64,7 +64,11 @@ typedef struct {
 /* One hop: the pinned query block (n_q rows) against a visiting key/value block
  * (n_k rows).  Only query rows [q_begin, q_begin+q_len) and key rows
  * [k_begin, k_begin+k_len) participate (zigzag hop classes).  With `causal`,
- * key j is visible to query i iff k_map(j) <= q_map(i) (masking.py:116-117). */
+ * key j is visible to query i iff k_map(j) <= q_map(i) (masking.py:116-117).
+ * With `grid_skip` != NULL (BlockGrid, masking.py:33-63 and 120-128), key j is
+ * also hidden from query i when cell (q_map(i) / grid_qcell, k_map(j) / grid_kcell)
+ * is skipped: grid_skip is a device array of grid_nqb * grid_nkb bytes, row-major
+ * over (query cell, key cell), 1 = skipped. */
 typedef struct {
   int32_t batch, heads, head_dim, dtype;
   int64_t n_q, n_k;
@@ -72,6 +76,9 @@ typedef struct {
   float softmax_scale;
   int32_t causal;
   burst_posmap q_map, k_map;
+  const uint8_t* grid_skip;
+  int32_t grid_nqb, grid_nkb;
+  int64_t grid_qcell, grid_kcell;
 } burst_hop;
 
 /* Elements (float) of one TL workspace for [batch, n, heads, head_dim]. */

@@ -60,6 +60,37 @@ def causal_allowed(q_pos: np.ndarray, k_pos: np.ndarray) -> np.ndarray:
     return k_pos[None, :] <= q_pos[:, None]
 
 
+class GridCells:
+    """Coarse block grid over the global score matrix (BlockGrid, masking.py:33-63):
+    n_query_blocks x n_key_blocks equal cells of a `total` x `total` matrix (validate
+    requires divisibility, masking.py:135-139); `skip` = set of (qb, kb) cells whose
+    scores are masked (allowed(), masking.py:120-128)."""
+
+    def __init__(self, n_query_blocks, n_key_blocks, skip, total):
+        self.nqb, self.nkb, self.total = int(n_query_blocks), int(n_key_blocks), int(total)
+        self.skip = frozenset((int(a), int(b)) for a, b in skip)
+        self.table = np.zeros((self.nqb, self.nkb), dtype=bool)
+        for a, b in self.skip:
+            self.table[a, b] = True
+
+    def allowed(self, q_pos: np.ndarray, k_pos: np.ndarray) -> np.ndarray:
+        qc = (np.asarray(q_pos) * self.nqb) // self.total
+        kc = (np.asarray(k_pos) * self.nkb) // self.total
+        return ~self.table[qc[:, None], kc[None, :]]
+
+
+def mask_allowed(q_pos, k_pos, causal=False, grid=None):
+    """Element map of the composed mask (BlockMask.allowed, masking.py:110-130) for
+    explicit global positions, or None when nothing is masked."""
+    out = None
+    if causal:
+        out = causal_allowed(np.asarray(q_pos), np.asarray(k_pos))
+    if grid is not None:
+        g = grid.allowed(q_pos, k_pos)
+        out = g if out is None else (out & g)
+    return out
+
+
 # ---------------------------------------------------------------------------
 # Partial (unnormalized) attention state -- PartialAttn (local_attn.py:66-135)
 # ---------------------------------------------------------------------------
@@ -114,7 +145,7 @@ def _block_partial(q, k, v, scale, allowed=None) -> Partial:
 
 
 def local_forward_tiled(q, k, v, scale, tile_rows=128, tile_cols=128,
-                        q_pos=None, k_pos=None, causal=False) -> Partial:
+                        q_pos=None, k_pos=None, causal=False, grid=None) -> Partial:
     """LAO forward over one (query block x key block) rectangle.
 
     Restates local_forward_tiled (local_attn.py:207-248): query tiles x key
@@ -126,7 +157,7 @@ def local_forward_tiled(q, k, v, scale, tile_rows=128, tile_cols=128,
     dt = q.dtype
     rows, d = q.shape
     out = Partial.empty(rows, v.shape[1], dt)
-    if causal:
+    if causal or grid is not None:
         assert q_pos is not None and k_pos is not None
     for r0 in range(0, rows, tile_rows):
         r1 = min(r0 + tile_rows, rows)
@@ -134,8 +165,8 @@ def local_forward_tiled(q, k, v, scale, tile_rows=128, tile_cols=128,
         for c0 in range(0, k.shape[0], tile_cols):
             c1 = min(c0 + tile_cols, k.shape[0])
             allowed = None
-            if causal:
-                allowed = causal_allowed(q_pos[r0:r1], k_pos[c0:c1])
+            if causal or grid is not None:
+                allowed = mask_allowed(q_pos[r0:r1], k_pos[c0:c1], causal, grid)
                 if not allowed.any():
                     continue
                 if allowed.all():
@@ -146,7 +177,7 @@ def local_forward_tiled(q, k, v, scale, tile_rows=128, tile_cols=128,
 
 
 def local_backward(q, k, v, do, lse, d_stat, scale, tile_rows=128, tile_cols=128,
-                   q_pos=None, k_pos=None, causal=False):
+                   q_pos=None, k_pos=None, causal=False, grid=None):
     """Gradient contributions of one rectangle (local_attn.py:255-289, tiled
     form _backward_tiled 313-353).  Returns (dQ, dK, dV) contributions."""
     dt = q.dtype
@@ -159,8 +190,8 @@ def local_backward(q, k, v, do, lse, d_stat, scale, tile_rows=128, tile_cols=128
         for c0 in range(0, k.shape[0], tile_cols):
             c1 = min(c0 + tile_cols, k.shape[0])
             allowed = None
-            if causal:
-                allowed = causal_allowed(q_pos[r0:r1], k_pos[c0:c1])
+            if causal or grid is not None:
+                allowed = mask_allowed(q_pos[r0:r1], k_pos[c0:c1], causal, grid)
                 if not allowed.any():
                     continue
             s = (q[r0:r1] * sc) @ k[c0:c1].T
@@ -182,12 +213,12 @@ def local_backward(q, k, v, do, lse, d_stat, scale, tile_rows=128, tile_cols=128
 # Dense oracle (dense.py:63-118)
 # ---------------------------------------------------------------------------
 
-def forward_dense(q, k, v, scale, causal=False):
+def forward_dense(q, k, v, scale, causal=False, grid=None):
     # _forward_arrays, dense.py:70-87
     s = (q * q.dtype.type(scale)) @ k.T
-    if causal:
-        n = q.shape[0]
-        s[~causal_allowed(np.arange(n), np.arange(k.shape[0]))] = -np.inf
+    allowed = mask_allowed(np.arange(q.shape[0]), np.arange(k.shape[0]), causal, grid)
+    if allowed is not None:
+        s[~allowed] = -np.inf
     m = s.max(axis=1)
     m_eff = np.where(np.isneginf(m), 0.0, m).astype(s.dtype)
     p = np.exp(s - m_eff[:, None])
@@ -199,12 +230,13 @@ def forward_dense(q, k, v, scale, causal=False):
     return o, lse
 
 
-def backward_dense(q, k, v, do, scale, causal=False):
+def backward_dense(q, k, v, do, scale, causal=False, grid=None):
     # backward_dense, dense.py:99-118
-    o, lse = forward_dense(q, k, v, scale, causal)
+    o, lse = forward_dense(q, k, v, scale, causal, grid)
     s = (q * q.dtype.type(scale)) @ k.T
-    if causal:
-        s[~causal_allowed(np.arange(q.shape[0]), np.arange(k.shape[0]))] = -np.inf
+    allowed = mask_allowed(np.arange(q.shape[0]), np.arange(k.shape[0]), causal, grid)
+    if allowed is not None:
+        s[~allowed] = -np.inf
     prob = np.exp(s - lse[:, None])
     d_stat = (do * o).sum(axis=1)
     dv = prob.T @ do
@@ -237,7 +269,7 @@ def zigzag_positions(n: int, G: int) -> list[np.ndarray]:
             for i in range(G)]
 
 
-def ring_forward(q, k, v, scale, G, causal=False, zigzag=False, tile=128):
+def ring_forward(q, k, v, scale, G, causal=False, zigzag=False, tile=128, grid=None):
     """Lockstep ring forward (sim.py:551-574 + ring.forward_step 158-181).
 
     Device i holds payload from origin (i - r) mod G at round r (sim.py:565,
@@ -250,10 +282,11 @@ def ring_forward(q, k, v, scale, G, causal=False, zigzag=False, tile=128):
         for i in range(G):
             j = (i - r) % G
             qp, kp = pos[i], pos[j]
-            if causal and not causal_allowed(qp, kp).any():
+            allowed = mask_allowed(qp, kp, causal, grid)
+            if allowed is not None and not allowed.any():
                 continue  # whole-hop SKIP (ring.py:169-171)
             part = local_forward_tiled(q[qp], k[kp], v[kp], scale, tile, tile,
-                                       qp, kp, causal)
+                                       qp, kp, causal, grid)
             states[i].merge(part)   # hop merge (ring.py:180)
     outs = []
     for i in range(G):
@@ -262,14 +295,14 @@ def ring_forward(q, k, v, scale, G, causal=False, zigzag=False, tile=128):
     return outs
 
 
-def ring_backward(q, k, v, do, scale, G, causal=False, zigzag=False, tile=128):
+def ring_backward(q, k, v, do, scale, G, causal=False, zigzag=False, tile=128, grid=None):
     """Lockstep ring backward (ring.init_backward 195-218, backward_step 221-242).
 
     Returns global (dQ, dK, dV, O, lse) assembled from all devices.
     """
     n = q.shape[0]
     pos = zigzag_positions(n, G) if zigzag else contiguous_positions(n, G)
-    fwd = ring_forward(q, k, v, scale, G, causal, zigzag, tile)
+    fwd = ring_forward(q, k, v, scale, G, causal, zigzag, tile, grid)
     o = np.zeros_like(q)
     lse = np.zeros(n, q.dtype)
     for p, oi, li in fwd:
@@ -282,10 +315,11 @@ def ring_backward(q, k, v, do, scale, G, causal=False, zigzag=False, tile=128):
         for i in range(G):
             j = (i - r) % G
             qp, kp = pos[i], pos[j]
-            if causal and not causal_allowed(qp, kp).any():
+            allowed = mask_allowed(qp, kp, causal, grid)
+            if allowed is not None and not allowed.any():
                 continue
             a, b, c = local_backward(q[qp], k[kp], v[kp], do[qp], lse[qp], d_stat[qp],
-                                     scale, tile, tile, qp, kp, causal)
+                                     scale, tile, tile, qp, kp, causal, grid)
             dq[qp] += a
             dk[kp] += b
             dv[kp] += c

@@ -34,7 +34,9 @@ class Hop(ctypes.Structure):
                 ("n_q", _c_i64), ("n_k", _c_i64),
                 ("q_begin", _c_i64), ("q_len", _c_i64), ("k_begin", _c_i64), ("k_len", _c_i64),
                 ("softmax_scale", _c_f32), ("causal", _c_i32),
-                ("q_map", PosMap), ("k_map", PosMap)]
+                ("q_map", PosMap), ("k_map", PosMap),
+                ("grid_skip", _c_p), ("grid_nqb", _c_i32), ("grid_nkb", _c_i32),
+                ("grid_qcell", _c_i64), ("grid_kcell", _c_i64)]
 
 
 class P2POp(ctypes.Structure):

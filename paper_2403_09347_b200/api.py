@@ -18,6 +18,7 @@ from dataclasses import dataclass
 import torch
 
 from .errors import ConfigError, ShapeError
+from .masks import GridMask
 from .kernels import CudaKernels, check_qkv, default_scale
 from .ring import (NcclTransport, SoloTransport, ring_backward, ring_backward_qtravel,
                    ring_forward, run_ranks)
@@ -51,28 +52,29 @@ def _transport_for(group):
 class _BurstAttnFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, q, k, v, scale, causal, zigzag, transport, kernels, n_valid, recorders,
-                bwd_payload):
+                bwd_payload, grid):
         rec_f, rec_b = recorders if recorders is not None else (None, None)
         o, lse = ring_forward(q, k, v, scale, causal, zigzag, transport, kernels, n_valid,
-                              recorder=rec_f)
+                              recorder=rec_f, grid=grid)
         ctx.save_for_backward(q, k, v, o, lse)
-        ctx.cfg = (scale, causal, zigzag, transport, kernels, n_valid, rec_b, bwd_payload)
+        ctx.cfg = (scale, causal, zigzag, transport, kernels, n_valid, rec_b, bwd_payload, grid)
         ctx.mark_non_differentiable(lse)
         return o, lse
 
     @staticmethod
     def backward(ctx, do, _dlse):
         q, k, v, o, lse = ctx.saved_tensors
-        scale, causal, zigzag, transport, kernels, n_valid, rec_b, bwd_payload = ctx.cfg
+        scale, causal, zigzag, transport, kernels, n_valid, rec_b, bwd_payload, grid = ctx.cfg
         bwd = ring_backward_qtravel if bwd_payload == "q" else ring_backward
         dq, dk, dv = bwd(q, k, v, o, lse, do.contiguous(), scale, causal, zigzag, transport,
-                         kernels, n_valid, recorder=rec_b)
-        return dq, dk, dv, None, None, None, None, None, None, None, None
+                         kernels, n_valid, recorder=rec_b, grid=grid)
+        return dq, dk, dv, None, None, None, None, None, None, None, None, None
 
 
 def burst_attn_func(q, k, v, causal: bool = False, softmax_scale: float | None = None,
                     group=None, zigzag: bool | None = None, valid_len: int | None = None, *,
-                    bwd_payload: str = "kv", _transport=None, _kernels=None, _recorders=None):
+                    bwd_payload: str = "kv", mask=None, _transport=None, _kernels=None,
+                    _recorders=None):
     """BurstAttention over the ranks of `group` (NCCL ring over NVLink).
 
     q, k, v: [batch, n_local, heads, head_dim] shards of the global sequence
@@ -85,6 +87,9 @@ def burst_attn_func(q, k, v, causal: bool = False, softmax_scale: float | None =
     `bwd_payload`: "kv" (default) rotates K/V and sends fp32 dK/dV contributions
     home; "q" is the reference's payload (Q, dO, lse/D travel, K/V/dK/dV pinned,
     ring.py:65-83) with fp32 dQ contributions sent home.
+    `mask`: block-sparse grid over the GLOBAL score matrix -- a masks.GridMask or a
+    mask_from_spec value (dict / JSON path with n_query_blocks, n_key_blocks, skip and
+    an optional causal flag; masking.py:150-180); composes with `causal`.
     `_recorders`: optional (forward, backward) trace.PassRecorder pair that
     records this rank's measured hop timeline and byte ledger.
     """
@@ -104,8 +109,26 @@ def burst_attn_func(q, k, v, causal: bool = False, softmax_scale: float | None =
         raise ShapeError(f"valid_len={valid_len} outside (0, {q.shape[1] * transport.world}]")
     if bwd_payload not in ("kv", "q"):
         raise ConfigError(f"bwd_payload must be 'kv' or 'q', got {bwd_payload!r}")
+    grid, causal = _bind_mask(mask, causal, valid_len or q.shape[1] * transport.world)
     return _BurstAttnFn.apply(q, k, v, scale, bool(causal), bool(zigzag), transport, kernels,
-                              valid_len, _recorders, bwd_payload)
+                              valid_len, _recorders, bwd_payload, grid)
+
+
+def _bind_mask(mask, causal, total):
+    """(GridMask bound to the global length or None, effective causal flag); validates
+    that every real query row keeps a visible key (BlockMask.validate, masking.py:132-147)."""
+    if mask is None:
+        return None, causal
+    if isinstance(mask, GridMask):
+        grid, spec_causal = mask, False
+    else:
+        grid, spec_causal = GridMask.from_spec(mask)
+    causal = bool(causal) or spec_causal
+    if grid is None:
+        return None, causal
+    grid = grid.bind(total)
+    grid.validate(causal)
+    return grid, causal
 
 
 @dataclass
@@ -122,7 +145,7 @@ class PassResult:
 def run_ring_pass(q, k, v, world: int, causal: bool = False, softmax_scale: float | None = None,
                   dout=None, zigzag: bool | None = None, kernels=None,
                   pad: bool = False, trace: bool = False,
-                  bwd_payload: str = "kv") -> PassResult:
+                  bwd_payload: str = "kv", mask=None) -> PassResult:
     """Whole-ring forward (+ backward when `dout` is given) of GLOBAL tensors
     [batch, N, heads, head_dim] over `world` simulated devices on this GPU.
 
@@ -159,6 +182,7 @@ def run_ring_pass(q, k, v, world: int, causal: bool = False, softmax_scale: floa
         q, k, v = padz(q), padz(k), padz(v)
         dout = padz(dout) if dout is not None else None
     scale = default_scale(q.shape[-1]) if softmax_scale is None else float(softmax_scale)
+    grid, causal = _bind_mask(mask, causal, N)   # cells tile the real length (padding excluded)
     shards = [[shard(t, r, world, zigzag) for r in range(world)] for t in (q, k, v)]
     do_sh = [shard(dout, r, world, zigzag) for r in range(world)] if dout is not None else None
 
@@ -168,12 +192,12 @@ def run_ring_pass(q, k, v, world: int, causal: bool = False, softmax_scale: floa
     def one(rank, transport):
         qs, ks, vs = shards[0][rank], shards[1][rank], shards[2][rank]
         o, lse = ring_forward(qs, ks, vs, scale, causal, zigzag, transport, kernels, n_valid,
-                              recorder=rec_f[rank])
+                              recorder=rec_f[rank], grid=grid)
         if do_sh is None:
             return o, lse, None
         bwd = ring_backward_qtravel if bwd_payload == "q" else ring_backward
         g = bwd(qs, ks, vs, o, lse, do_sh[rank], scale, causal, zigzag, transport, kernels,
-                n_valid, recorder=rec_b[rank])
+                n_valid, recorder=rec_b[rank], grid=grid)
         return o, lse, g
 
     res = run_ranks(world, one)

@@ -123,6 +123,10 @@ int check_hop(const burst_hop* h) {
     return fail(BURST_E_SHAPE, "hop row ranges exceed the q/k extents");
   if (!(h->softmax_scale > 0.f)) return fail(BURST_E_SHAPE, "softmax_scale must be finite and positive");
   if (h->n_q > INT32_MAX || h->n_k > INT32_MAX) return fail(BURST_E_SHAPE, "sequence too long for TMA coordinates");
+  if (h->grid_skip && (h->grid_nqb < 1 || h->grid_nkb < 1 || h->grid_qcell < 1 || h->grid_kcell < 1))
+    return fail(BURST_E_SHAPE, "grid mask needs positive block counts and cell extents");
+  if (h->grid_skip && (!valid_map(h->q_map) || !valid_map(h->k_map)))
+    return fail(BURST_E_SHAPE, "position maps must be monotone (pos0 + seg_len <= pos1)");
   if (h->causal && (!valid_map(h->q_map) || !valid_map(h->k_map)))
     return fail(BURST_E_SHAPE, "position maps must be monotone (pos0 + seg_len <= pos1)");
   if (h->dtype == BURST_DTYPE_BF16) {

@@ -24,6 +24,49 @@ __host__ __device__ __forceinline__ int64_t count_le(const burst_posmap& m, int6
   return c < n ? c : n;
 }
 
+// Block-sparse grid (BlockGrid, masking.py:33-63, 120-128): is the cell of
+// (query position qp, key position kp) skipped?
+// Cell indices are clamped: zero-padded rows (positions >= the real length the grid
+// tiles) read the last cell; their results are discarded by the caller.
+__device__ __forceinline__ int64_t grid_qc(const burst_hop& h, int64_t qp) {
+  const int64_t c = qp / h.grid_qcell;
+  return c < h.grid_nqb ? c : h.grid_nqb - 1;
+}
+__device__ __forceinline__ int64_t grid_kc(const burst_hop& h, int64_t kp) {
+  const int64_t c = kp / h.grid_kcell;
+  return c < h.grid_nkb ? c : h.grid_nkb - 1;
+}
+__device__ __forceinline__ bool grid_skipped(const burst_hop& h, int64_t qp, int64_t kp) {
+  return h.grid_skip[grid_qc(h, qp) * h.grid_nkb + grid_kc(h, kp)] != 0;
+}
+
+// Grid-mask bits of a run of `n` (<= 64) consecutive local key rows [k0, k0+n) for one
+// query position: bit i set = key k0+i hidden.  One table lookup when the run stays in
+// one key cell (the common case), per key otherwise.
+__device__ __forceinline__ uint64_t grid_key_bits(const burst_hop& h, int64_t qp, int64_t k0, int n) {
+  const int64_t row = grid_qc(h, qp) * h.grid_nkb;
+  const int64_t kp0 = pos_of(h.k_map, k0), kp1 = pos_of(h.k_map, k0 + n - 1);
+  if (kp1 - kp0 == n - 1 && grid_kc(h, kp0) == grid_kc(h, kp1))
+    return h.grid_skip[row + grid_kc(h, kp0)] ? (n == 64 ? ~0ull : ((1ull << n) - 1)) : 0ull;
+  uint64_t bits = 0;
+  for (int i = 0; i < n; ++i)
+    if (h.grid_skip[row + grid_kc(h, pos_of(h.k_map, k0 + i))]) bits |= 1ull << i;
+  return bits;
+}
+
+// Same for a run of `n` (<= 64) consecutive local query rows against one key position.
+__device__ __forceinline__ uint64_t grid_query_bits(const burst_hop& h, int64_t q0, int n, int64_t kp) {
+  const int64_t col = grid_kc(h, kp);
+  const int64_t qp0 = pos_of(h.q_map, q0), qp1 = pos_of(h.q_map, q0 + n - 1);
+  if (qp1 - qp0 == n - 1 && grid_qc(h, qp0) == grid_qc(h, qp1))
+    return h.grid_skip[grid_qc(h, qp0) * h.grid_nkb + col] ? (n == 64 ? ~0ull : ((1ull << n) - 1))
+                                                          : 0ull;
+  uint64_t bits = 0;
+  for (int i = 0; i < n; ++i)
+    if (h.grid_skip[grid_qc(h, pos_of(h.q_map, q0 + i)) * h.grid_nkb + col]) bits |= 1ull << i;
+  return bits;
+}
+
 // Tile-interleaved fp32 workspace layout (O_acc, dQ_acc, dK/dV contributions):
 // [B*H][ceil(n/128)][D/4][128 rows][4 cols].  A warp whose lanes own 32
 // consecutive rows touches one contiguous 512 B run per float4 column group,

@@ -303,7 +303,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const int64_t krow = k0 + t;
     const bool kvalid = krow < k_end && krow < hp.n_k;
-    const int64_t kpos = hp.causal ? pos_of(hp.k_map, kvalid ? krow : k0) : 0;
+    const int64_t kpos = (hp.causal || hp.grid_skip) ? pos_of(hp.k_map, kvalid ? krow : k0) : 0;
     const int64_t qfirst = hp.causal ? count_le(hp.q_map, hp.n_q, kpos - 1) : 0;
     const float c2 = p.scale_log2;
     const uint32_t p_bar = ptx::leader_addr(bar + B_P), ds_bar = ptx::leader_addr(bar + B_DS);
@@ -319,7 +319,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int64_t lo64 = qfirst - q0, hi64 = q_end - q0;
       const int lo = lo64 < 0 ? 0 : (lo64 > BM ? BM : (int)lo64);
       const int hi = !kvalid ? 0 : (hi64 > BM ? BM : (hi64 < 0 ? 0 : (int)hi64));
-      const bool warp_full = __all_sync(0xffffffffu, lo == 0 && hi == BM);
+      uint64_t gq0 = 0, gq1 = 0;   // block-sparse grid: hidden query columns
+      if (hp.grid_skip) {
+        const int nv = hi64 > BM ? BM : (hi64 < 0 ? 0 : (int)hi64);
+        if (nv > 0) gq0 = grid_query_bits(hp, q0, nv < 64 ? nv : 64, kpos);
+        if (nv > 64) gq1 = grid_query_bits(hp, q0 + 64, nv - 64, kpos);
+      }
+      const bool warp_full = __all_sync(0xffffffffu, lo == 0 && hi == BM && (gq0 | gq1) == 0);
       ptx::mbar_wait(bar + B_ST_F + s, (i / kStatSlots) & 1);
       ptx::mbar_wait(bar + B_S, i & 1); BTRACE2(3, i);
       ptx::tc_fence_after();
@@ -345,7 +351,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (!warp_full) {
 #pragma unroll
         for (int c = 0; c < BM; ++c)
-          if (c < lo || c >= hi) pr[c] = 0.f;
+          if (c < lo || c >= hi || (((c < 64 ? gq0 : gq1) >> (c & 63)) & 1)) pr[c] = 0.f;
       }
 #pragma unroll
       for (int cc = 0; cc < BM / 64; ++cc) {

@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const int64_t krow = k0 + t;
     const bool kvalid = krow < k_end && krow < hp.n_k;
-    const int64_t kpos = hp.causal ? pos_of(hp.k_map, kvalid ? krow : k0) : 0;
+    const int64_t kpos = (hp.causal || hp.grid_skip) ? pos_of(hp.k_map, kvalid ? krow : k0) : 0;
     const int64_t qfirst = hp.causal ? count_le(hp.q_map, hp.n_q, kpos - 1) : 0;
     const float c2 = p.scale_log2;
     for (int i = 0; i < nq; ++i) {
@@ -345,7 +345,12 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
       int64_t lo64 = qfirst - q0, hi64 = q_end - q0;
       const int lo = lo64 < 0 ? 0 : (lo64 > 64 ? 64 : (int)lo64);
       const int hi = !kvalid ? 0 : (hi64 > 64 ? 64 : (hi64 < 0 ? 0 : (int)hi64));
-      const bool warp_full = __all_sync(0xffffffffu, lo == 0 && hi == 64);
+      uint64_t gq = 0;   // block-sparse grid: hidden query columns of this half
+      if (hp.grid_skip) {
+        const int nv = hi64 > 64 ? 64 : (hi64 < 0 ? 0 : (int)hi64);
+        if (nv > 0) gq = grid_query_bits(hp, q0, nv, kpos);
+      }
+      const bool warp_full = __all_sync(0xffffffffu, lo == 0 && hi == 64 && gq == 0);
       ptx::mbar_wait(qdo_full + s, (i >> 1) & 1);
       ptx::mbar_wait(s_full, i & 1); if (hq == 0) BTRACE4(3, i);
       ptx::tc_fence_after();
@@ -372,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
       if (!warp_full) {
 #pragma unroll
         for (int c = 0; c < 64; ++c)
-          if (c < lo || c >= hi) pr[c] = 0.f;
+          if (c < lo || c >= hi || ((gq >> c) & 1)) pr[c] = 0.f;
       }
       {
         uint32_t pk[32];

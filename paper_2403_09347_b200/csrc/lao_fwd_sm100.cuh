@@ -222,6 +222,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
     const bool valid = row < q_end && row < hp.n_q;
     // keys visible to this row, relative to the hop's k_begin
     int64_t lim = hp.k_len;
+    const int64_t qpos = pos_of(hp.q_map, valid ? row : (q_end - 1 > row0 ? q_end - 1 : row0));
     if (hp.causal) {
       int64_t cnt = count_le(hp.k_map, hp.n_k, pos_of(hp.q_map, valid ? row : q_end - 1)) -
                     hp.k_begin;
@@ -245,11 +246,18 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
         for (int i = 0; i < BN; ++i) s[i] = __uint_as_float(r[i]);
       }
       const int64_t nvalid = lim - (int64_t)j * BN;
-      const bool partial = __any_sync(0xffffffffu, nvalid < BN);
+      uint64_t gk0 = 0, gk1 = 0;   // block-sparse grid: hidden key columns of this row
+      if (hp.grid_skip) {
+        const int nv = nvalid > BN ? BN : (nvalid < 0 ? 0 : (int)nvalid);
+        const int64_t kt0 = hp.k_begin + (int64_t)j * BN;
+        if (nv > 0) gk0 = grid_key_bits(hp, qpos, kt0, nv < 64 ? nv : 64);
+        if (nv > 64) gk1 = grid_key_bits(hp, qpos, kt0 + 64, nv - 64);
+      }
+      const bool partial = __any_sync(0xffffffffu, nvalid < BN || (gk0 | gk1) != 0);
       if (partial) {
 #pragma unroll
         for (int i = 0; i < BN; ++i)
-          if (i >= nvalid) s[i] = -INFINITY;
+          if (i >= nvalid || (((i < 64 ? gk0 : gk1) >> (i & 63)) & 1)) s[i] = -INFINITY;
       }
       // row max as 8 independent chains (a single chain is 128 dependent FMNMX)
       float mx8[8];

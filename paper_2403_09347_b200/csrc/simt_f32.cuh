@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(kRows) simt_fwd_kernel(const FwdParams p) {
   const int64_t row = row0 + t;
   const bool valid = row < q_end;
   const int64_t bh = (int64_t)b * hp.heads + h;
+  const int64_t qpos = pos_of(hp.q_map, valid ? row : (q_end > 0 ? q_end - 1 : 0));
 
   int64_t kspan = hp.k_len, lim = hp.k_len;
   if (hp.causal) {
@@ -76,7 +77,9 @@ __global__ void __launch_bounds__(kRows) simt_fwd_kernel(const FwdParams p) {
       float acc = 0.f;
 #pragma unroll
       for (int c = 0; c < D; ++c) acc = fmaf(q[c], sk[j][c], acc);
-      s[j] = (k0 + j < lim) ? acc * p.scale_log2 : -INFINITY;
+      const bool hidden = k0 + j >= lim ||
+          (hp.grid_skip && grid_skipped(hp, qpos, pos_of(hp.k_map, hp.k_begin + k0 + j)));
+      s[j] = hidden ? -INFINITY : acc * p.scale_log2;
       mx = fmaxf(mx, s[j]);
     }
     const float m_new = fmaxf(m, mx);
@@ -154,6 +157,7 @@ __global__ void __launch_bounds__(kRows) simt_bwd_dq_kernel(const BwdParams p) {
   const bool valid = row < q_end;
   const int64_t bh = (int64_t)b * hp.heads + h;
   const int64_t NTq = ceil_div(hp.n_q, 128);
+  const int64_t qpos = pos_of(hp.q_map, valid ? row : (q_end > 0 ? q_end - 1 : 0));
   int64_t kspan = hp.k_len, lim = hp.k_len;
   if (hp.causal) {
     const int64_t last = (row0 + kRows < q_end ? row0 + kRows : q_end) - 1;
@@ -186,6 +190,7 @@ __global__ void __launch_bounds__(kRows) simt_bwd_dq_kernel(const BwdParams p) {
 #pragma unroll 4
     for (int j = 0; j < kTile; ++j) {
       if (k0 + j >= lim) continue;
+      if (hp.grid_skip && grid_skipped(hp, qpos, pos_of(hp.k_map, hp.k_begin + k0 + j))) continue;
       float s = 0.f, dp = 0.f;
 #pragma unroll
       for (int c = 0; c < D; ++c) {
@@ -229,6 +234,7 @@ __global__ void __launch_bounds__(kRows) simt_bwd_dkv_kernel(const BwdParams p) 
     const int64_t g = count_le(hp.q_map, hp.n_q, pos_of(hp.k_map, valid ? krow : k0) - 1);
     qfirst = g > qfirst ? g : qfirst;
   }
+  const int64_t kposg = pos_of(hp.k_map, valid ? krow : k0);
   float kr[D], vr[D];
 #pragma unroll
   for (int c = 0; c < D; ++c) {
@@ -258,6 +264,7 @@ __global__ void __launch_bounds__(kRows) simt_bwd_dkv_kernel(const BwdParams p) 
     if (!valid) continue;
     for (int j = 0; j < kTile; ++j) {
       if (q0 + j < qfirst || q0 + j >= q_end) continue;
+      if (hp.grid_skip && grid_skipped(hp, pos_of(hp.q_map, q0 + j), kposg)) continue;
       float s = 0.f, dp = 0.f;
 #pragma unroll
       for (int c = 0; c < D; ++c) {

@@ -94,6 +94,12 @@ def make_hop(plan: HopPlan, q: torch.Tensor, k: torch.Tensor, scale: float) -> _
     h.causal = 1 if plan.causal else 0
     h.q_map = _lib.PosMap(plan.q_map.pos0, plan.q_map.pos1, plan.q_map.seg_len)
     h.k_map = _lib.PosMap(plan.k_map.pos0, plan.k_map.pos1, plan.k_map.seg_len)
+    g = plan.grid
+    if g is not None:
+        # keeps the table alive: GridMask.device_table caches it per device
+        h.grid_skip = g.device_table(q.device).data_ptr()
+        h.grid_nqb, h.grid_nkb = g.n_query_blocks, g.n_key_blocks
+        h.grid_qcell, h.grid_kcell = g.qcell, g.kcell
     return h
 
 
@@ -188,6 +194,12 @@ class CudaKernels:
         self.tl_sum([st.dq_acc] + list(dq_parts), dq, stream)
         self.tl_sum([dk_acc], dk, stream)
         self.tl_sum([dv_acc], dv, stream)
+
+    def zero_(self, bufs, stream=None) -> None:
+        """Zero contribution buffers on `stream` (a fully masked own block)."""
+        with torch.cuda.stream(stream) if stream is not None else _nullctx():
+            for b in bufs:
+                b.zero_()
 
     def read_flags(self, stream=None) -> int:
         out = ctypes.c_int32(0)

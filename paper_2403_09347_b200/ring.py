@@ -252,10 +252,11 @@ class LoopbackTransport:
 # ---------------------------------------------------------------------------
 
 def ring_forward(q, k, v, scale: float, causal: bool, zigzag: bool, transport, kernels,
-                 n_valid: int | None = None, recorder=None):
+                 n_valid: int | None = None, recorder=None, grid=None):
     """One rank's forward pass.  Returns (O [B,n,H,D], lse [B,H,n] natural log).
     `n_valid`: real global length when the shards are zero-padded (reference pad=True).
-    `recorder`: optional trace.PassRecorder (measured timeline + ledger, sim.py:118-261)."""
+    `recorder`: optional trace.PassRecorder (measured timeline + ledger, sim.py:118-261).
+    `grid`: optional masks.GridMask bound to the global length (BlockGrid)."""
     B, n, H, D = q.shape
     G, r = transport.world, transport.rank
     S = _Streams(q.device)
@@ -265,9 +266,10 @@ def ring_forward(q, k, v, scale: float, causal: bool, zigzag: bool, transport, k
     cur_k, cur_v = k, v
     spare = None
     finalized = False
+    computed = False             # a hop has merged into the running state
     prev = S.compute_mark()      # compute tail before hop h (buffers it still reads)
     for h in range(G):
-        plan = plan_hop(r, G, h, n, causal, zigzag, n_valid)
+        plan = plan_hop(r, G, h, n, causal, zigzag, n_valid, grid)
         exchanged = False
         # launch the hop's kernel first, then post the transfer on the comm stream:
         # both run concurrently (the comm waits only for the PREVIOUS hop's kernel,
@@ -276,9 +278,10 @@ def ring_forward(q, k, v, scale: float, causal: bool, zigzag: bool, transport, k
             recorder.mark(h, "compute_start", S.compute)
         if not plan.skip:
             fin = h == G - 1 and plan.covers_all_queries(n)
-            kernels.fwd(plan, q, cur_k, cur_v, scale, state, o, lse, first=(h == 0), finalize=fin,
-                        stream=S.compute)
+            kernels.fwd(plan, q, cur_k, cur_v, scale, state, o, lse, first=not computed,
+                        finalize=fin, stream=S.compute)
             finalized = finalized or fin
+            computed = True
         if recorder is not None:
             recorder.mark(h, "compute_end", S.compute)
         done = S.compute_mark()
@@ -308,14 +311,14 @@ def ring_forward(q, k, v, scale: float, causal: bool, zigzag: bool, transport, k
 
 
 def _part_exchange(r: int, G: int, n: int, causal: bool, zigzag: bool, hop: int, send_bufs,
-                   kernels, like_k, like_v, n_valid=None):
+                   kernels, like_k, like_v, n_valid=None, grid=None):
     """Ops moving the dK/dV contribution computed at `hop` to its home rank."""
     ops, recv_bufs = [], None
-    mine = plan_hop(r, G, hop, n, causal, zigzag, n_valid)
+    mine = plan_hop(r, G, hop, n, causal, zigzag, n_valid, grid)
     if not mine.skip:
         ops += [(SEND, send_bufs[0], mine.src), (SEND, send_bufs[1], mine.src)]
     c = contributor_to(r, G, hop)
-    theirs = plan_hop(c, G, hop, n, causal, zigzag, n_valid)
+    theirs = plan_hop(c, G, hop, n, causal, zigzag, n_valid, grid)
     if not theirs.skip:
         recv_bufs = (kernels.part(like_k), kernels.part(like_v))
         ops += [(RECV, recv_bufs[0], c), (RECV, recv_bufs[1], c)]
@@ -323,7 +326,7 @@ def _part_exchange(r: int, G: int, n: int, causal: bool, zigzag: bool, hop: int,
 
 
 def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: bool, transport,
-                  kernels, n_valid: int | None = None, recorder=None):
+                  kernels, n_valid: int | None = None, recorder=None, grid=None):
     """One rank's backward pass.  Returns (dq, dk, dv) in q's dtype.
     `recorder`: optional trace.PassRecorder (see ring_forward)."""
     B, n, H, D = q.shape
@@ -338,7 +341,7 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
     spare = None
     prev = S.compute_mark()
     for h in range(G):
-        plan = plan_hop(r, G, h, n, causal, zigzag, n_valid)
+        plan = plan_hop(r, G, h, n, causal, zigzag, n_valid, grid)
         # the hop's kernel first, then the transfers (which wait only for hop h-1's
         # kernel: it produced the contribution sent now and last read `spare`)
         if recorder is not None:
@@ -352,6 +355,8 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
         if not plan.skip:
             kernels.bwd(plan, q, cur_k, cur_v, dout, scale, st, target[0], target[1],
                         accumulate=False, stream=S.compute)
+        elif h == 0:                  # own block fully masked (grid): no contribution
+            kernels.zero_(target, stream=S.compute)
         if recorder is not None:
             recorder.mark(h, "compute_end", S.compute)
         done = S.compute_mark()
@@ -363,7 +368,7 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
                     (RECV, spare[0], (r - 1) % G), (RECV, spare[1], (r - 1) % G)]
         if h >= 2:
             p_ops, got = _part_exchange(r, G, n, causal, zigzag, h - 1, send[(h - 1) % 2],
-                                        kernels, k, v, n_valid)
+                                        kernels, k, v, n_valid, grid)
             ops += p_ops
             if got is not None:
                 received.append(got)
@@ -389,7 +394,7 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
                 spare = None
     if G > 1:
         p_ops, got = _part_exchange(r, G, n, causal, zigzag, G - 1, send[(G - 1) % 2], kernels,
-                                    k, v, n_valid)
+                                    k, v, n_valid, grid)
         if got is not None:
             received.append(got)
         S.comm_after_compute()
@@ -408,22 +413,23 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
 
 
 def _qpart_exchange(r: int, G: int, n: int, causal: bool, zigzag: bool, hop: int, send_buf,
-                    kernels, like_q, n_valid=None):
+                    kernels, like_q, n_valid=None, grid=None):
     """Ops moving the dQ contribution computed at `hop` (for the visiting query
     block) to that block's home rank, and receiving the one computed for ours."""
     ops, recv_buf = [], None
     src = (r - hop) % G                        # origin of the query block I processed
-    if not plan_hop(src, G, (src - r) % G, n, causal, zigzag, n_valid).skip:
+    if not plan_hop(src, G, (src - r) % G, n, causal, zigzag, n_valid, grid).skip:
         ops.append((SEND, send_buf, src))
     c = (r + hop) % G                          # the rank that processed MY block at `hop`
-    if not plan_hop(r, G, (r - c) % G, n, causal, zigzag, n_valid).skip:
+    if not plan_hop(r, G, (r - c) % G, n, causal, zigzag, n_valid, grid).skip:
         recv_buf = kernels.dq_part(like_q)
         ops.append((RECV, recv_buf, c))
     return ops, recv_buf
 
 
 def ring_backward_qtravel(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: bool,
-                          transport, kernels, n_valid: int | None = None, recorder=None):
+                          transport, kernels, n_valid: int | None = None, recorder=None,
+                          grid=None):
     """One rank's backward pass with the REFERENCE's payload:
     the query-side record (Q, dO, lse/D statistics) travels the ring and K/V/dK/dV
     stay pinned (BackwardBody ring.py:65-83, backward_step ring.py:221-242,
@@ -447,7 +453,7 @@ def ring_backward_qtravel(q, k, v, o, lse, dout, scale: float, causal: bool, zig
     prev = S.compute_mark()
     for h in range(G):
         src = (r - h) % G
-        plan = plan_hop(src, G, (src - r) % G, n, causal, zigzag, n_valid)
+        plan = plan_hop(src, G, (src - r) % G, n, causal, zigzag, n_valid, grid)
         if recorder is not None:
             recorder.mark(h, "compute_start", S.compute)
         if h == 0:
@@ -470,7 +476,7 @@ def ring_backward_qtravel(q, k, v, o, lse, dout, scale: float, causal: bool, zig
             ops += [(RECV, t, (r - 1) % G) for t in spare]
         if h >= 2:
             p_ops, got = _qpart_exchange(r, G, n, causal, zigzag, h - 1, send[(h - 1) % 2],
-                                         kernels, q, n_valid)
+                                         kernels, q, n_valid, grid)
             ops += p_ops
             if got is not None:
                 received.append(got)
@@ -492,11 +498,10 @@ def ring_backward_qtravel(q, k, v, o, lse, dout, scale: float, causal: bool, zig
             if spare[0] is q:
                 spare = None   # never receive into the caller's tensors
     if first_kv:                                  # every hop skipped: no key is visible
-        for t in (dk_acc, dv_acc):
-            t.zero_()
+        kernels.zero_((dk_acc, dv_acc), stream=S.compute)
     if G > 1:
         p_ops, got = _qpart_exchange(r, G, n, causal, zigzag, G - 1, send[(G - 1) % 2], kernels,
-                                     q, n_valid)
+                                     q, n_valid, grid)
         if got is not None:
             received.append(got)
         S.comm_after_compute()

@@ -50,6 +50,7 @@ class HopPlan:
     causal: bool        # element-level causal mask inside the rectangle
     q_map: PosMap
     k_map: PosMap
+    grid: object = None  # masks.GridMask (bound) applied element-wise, or None
 
     @property
     def skip(self) -> bool:
@@ -89,7 +90,28 @@ def valid_rows(rank: int, world: int, n_local: int, zigzag: bool, n_valid: int |
 
 
 def plan_hop(rank: int, world: int, hop: int, n_local: int, causal: bool,
-             zigzag: bool, n_valid: int | None = None) -> HopPlan:
+             zigzag: bool, n_valid: int | None = None, grid=None) -> HopPlan:
+    """Rectangle of one hop, with an optional block-sparse grid (masks.GridMask,
+    bound to the global length): a rectangle whose every (query cell, key cell)
+    pair is skipped becomes SKIP (BlockMask.decision, masking.py:79-106), any
+    other keeps the grid for element-level masking in the kernels."""
+    plan = _plan_hop(rank, world, hop, n_local, causal, zigzag, n_valid)
+    if grid is None or plan.skip:
+        return plan
+    qp = plan.q_map.positions(plan.q_begin + plan.q_len)[plan.q_begin:]
+    kp = plan.k_map.positions(plan.k_begin + plan.k_len)[plan.k_begin:]
+    if not qp or not kp:
+        return plan
+    qc = sorted({p // grid.qcell for p in qp})
+    kc = sorted({p // grid.kcell for p in kp})
+    if all((a, b) in grid.skip for a in qc for b in kc):
+        return HopPlan(hop, rank, plan.src, SKIP, 0, 0, 0, 0, False, plan.q_map, plan.k_map)
+    from dataclasses import replace
+    return replace(plan, grid=grid)
+
+
+def _plan_hop(rank: int, world: int, hop: int, n_local: int, causal: bool,
+              zigzag: bool, n_valid: int | None = None) -> HopPlan:
     """Rectangle of one hop.  With padding (n_valid = real global length), padded
     keys are excluded by shortening the key range (BlockMask.with_padding,
     masking.py:74-75); under the causal rule they are invisible to every real

@@ -56,8 +56,12 @@ def ring_case(name, seq, dim, heads, gpus, precision, mask=None, tile=None, seed
     v = np.stack([p.V.array for p in problems])
     g = np.stack([m.array for m in do])
     out["input_checksum"] = _checksum([q, k, v, g])
-    out["meta"] = np.array([seq, dim, heads, gpus, seed, 1 if mask == "causal" else 0,
+    is_causal = mask == "causal" or (isinstance(mask, dict) and bool(mask.get("causal")))
+    out["meta"] = np.array([seq, dim, heads, gpus, seed, 1 if is_causal else 0,
                             tile or 0, 1 if precision == "single" else 2])
+    if isinstance(mask, dict):     # block-sparse grid (BlockGrid, masking.py:33-63)
+        out["grid"] = np.array([mask["n_query_blocks"], mask["n_key_blocks"]])
+        out["grid_skip"] = np.array(mask["skip"], dtype=np.int64).reshape(-1, 2)
     # dense oracle on the same inputs, for the tolerance the reference accepts
     if seq <= 256:
         dq = [backward_dense(p, m) for p, m in zip(problems, do)]
@@ -92,7 +96,24 @@ def lao_case(name, rows, cols, dim, row_offset, col_offset, n_total, causal, see
     print("wrote", name)
 
 
+def grid_cases():
+    """Block-sparse grid masks through the whole ring (mask_from_spec dict form,
+    masking.py:150-180), with and without the causal constraint."""
+    ring_case("ring_n64_d16_h2_g4_grid_f64", 64, 16, 2, 4, "double",
+              mask={"n_query_blocks": 4, "n_key_blocks": 4,
+                    "skip": [[0, 3], [2, 1], [1, 1], [3, 0]]}, tile=8, seed=11)
+    ring_case("ring_n128_d16_h1_g4_grid_causal_f64", 128, 16, 1, 4, "double",
+              mask={"n_query_blocks": 8, "n_key_blocks": 8, "causal": True,
+                    "skip": [[3, 1], [5, 2], [7, 0], [6, 6], [2, 0]]}, tile=16, seed=12)
+    ring_case("ring_n256_d32_h1_g2_grid_causal_f32", 256, 32, 1, 2, "single",
+              mask={"n_query_blocks": 4, "n_key_blocks": 4, "causal": True,
+                    "skip": [[1, 0], [3, 2]]}, tile=64, seed=13)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "grid":
+        grid_cases()
+        sys.exit(0)
     # BASELINE.json configs[0]: seq 1024, d 64, 2 heads, G 2, fp32, non-causal.
     # 128x128 tiles (the default SRAM tile gives identical math, 100x slower).
     ring_case("c1_seq1024_d64_h2_g2_f32", 1024, 64, 2, 2, "single", tile=128)
@@ -109,3 +130,4 @@ if __name__ == "__main__":
     # LAO rectangles in global coordinates (row/col offsets), causal partial tiles
     lao_case("lao_r12_c20_d8_causal", 12, 20, 8, 16, 4, 40, True, 7)
     lao_case("lao_r16_c16_d8_full", 16, 16, 8, 0, 16, 32, False, 8)
+    grid_cases()

@@ -18,6 +18,14 @@ def _np(t):
     return t.detach().double().cpu().numpy()
 
 
+def _grid(plan):
+    """The product's GridMask as the oracle's GridCells (same BlockGrid semantics)."""
+    g = plan.grid
+    if g is None:
+        return None
+    return orc.GridCells(g.n_query_blocks, g.n_key_blocks, g.skip, g.total)
+
+
 class OracleKernels:
     name = "oracle"
 
@@ -43,7 +51,8 @@ class OracleKernels:
         for b in range(B):
             for h in range(H):
                 part = orc.local_forward_tiled(qn[b, qs, h], kn[b, ks, h], vn[b, ks, h], scale,
-                                               128, 128, qp[qs], kp[ks], plan.causal)
+                                               128, 128, qp[qs], kp[ks], plan.causal,
+                                               _grid(plan))
                 if first:
                     acc = part
                 else:
@@ -88,7 +97,7 @@ class OracleKernels:
                 dq, dk, dv = orc.local_backward(qn[b, qs, h], kn[b, ks, h], vn[b, ks, h],
                                                 dn[b, qs, h], st["lse"][b, h, qs],
                                                 st["D"][b, h, qs], scale, 128, 128, qp[qs],
-                                                kp[ks], plan.causal)
+                                                kp[ks], plan.causal, _grid(plan))
                 st["dq"][b, qs, h] += dq
                 dk_part[b, ks, h] += torch.from_numpy(dk)
                 dv_part[b, ks, h] += torch.from_numpy(dv)
@@ -116,3 +125,7 @@ class OracleKernels:
         dq.copy_(tot.to(dq.dtype))
         dk.copy_(dk_acc.to(dk.dtype))
         dv.copy_(dv_acc.to(dv.dtype))
+
+    def zero_(self, bufs, stream=None):
+        for b in bufs:
+            b.zero_()

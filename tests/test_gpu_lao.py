@@ -125,6 +125,73 @@ def test_f32_reference_payload_rel_1e5():
         assert rel_err(got, ref) < 1e-5
 
 
+def _grid_oracle(q, k, v, do, world, causal, zigzag, spec):
+    """oracle_ring with a block-sparse grid (oracle GridCells = BlockGrid semantics)."""
+    from oracle import burst_oracle as orc
+    B, N, H, D = q.shape
+    grid = orc.GridCells(spec["n_query_blocks"], spec["n_key_blocks"], spec["skip"], N)
+    f = lambda t: t.float().cpu().numpy().astype(np.float64)
+    qn, kn, vn, dn = f(q), f(k), f(v), f(do)
+    out = [np.zeros((B, N, H, D)) for _ in range(4)]
+    for b in range(B):
+        for h in range(H):
+            dq, dk, dv, o, _ = orc.ring_backward(qn[b, :, h], kn[b, :, h], vn[b, :, h],
+                                                 dn[b, :, h], D ** -0.5, world, causal, zigzag,
+                                                 128, grid)
+            for t, x in zip(out, (o, dq, dk, dv)):
+                t[b, :, h] = x
+    return out
+
+
+GRID_SPECS = [
+    # 128-aligned cells, non-causal, a skipped diagonal cell (own block fully masked)
+    (1024, 2, False, False, {"n_query_blocks": 8, "n_key_blocks": 8,
+                             "skip": [[0, 0], [1, 5], [2, 2], [3, 7], [6, 1], [7, 7], [4, 4]]}),
+    # 96-row cells: cells straddle 128-row tiles (per-element path), causal zigzag
+    (768, 2, True, True, {"n_query_blocks": 8, "n_key_blocks": 8,
+                          "skip": [[3, 1], [5, 2], [7, 0], [6, 6], [2, 0], [4, 3]]}),
+    # own blocks of ranks 0 and 2 fully masked: hop 0 is SKIP (zeroed contribution,
+    # forward state starts at the first computed hop)
+    (1024, 4, False, False, {"n_query_blocks": 4, "n_key_blocks": 4, "skip": [[0, 0], [2, 2]]}),
+    # rectangular grid, causal contiguous, 4 ranks
+    (1024, 4, True, False, {"n_query_blocks": 4, "n_key_blocks": 8,
+                            "skip": [[1, 0], [2, 3], [3, 1], [3, 6]]}),
+]
+
+
+@pytest.mark.parametrize("N,world,causal,zigzag,spec", GRID_SPECS)
+@pytest.mark.parametrize("payload", ["kv", "q"])
+def test_bf16_grid_mask(N, world, causal, zigzag, spec, payload):
+    """Block-sparse grid masks (BlockGrid, masking.py:33-147) on the bf16 kernels."""
+    from paper_2403_09347_b200 import run_ring_pass
+    q, k, v, do = make_inputs(1, N, 2, 128, seed=N + world)
+    poison_allocator()
+    res = run_ring_pass(q, k, v, world, causal=causal, dout=do, zigzag=zigzag,
+                        mask=spec, bwd_payload=payload)
+    torch.cuda.synchronize()
+    o, dq, dk, dv = _grid_oracle(q, k, v, do, world, causal, zigzag, spec)
+    for name, got, ref in (("o", res.out, o), ("dq", res.dq, dq), ("dk", res.dk, dk),
+                           ("dv", res.dv, dv)):
+        assert max_abs(got, ref) < BF16_TOL, name
+
+
+def test_f32_grid_mask_vs_reference_golden(golden):
+    """f32 path with a causal grid mask against the reference's own outputs, 1e-5 rel."""
+    from oracle import burst_oracle as orc
+    from paper_2403_09347_b200 import run_ring_pass
+    g = golden("ring_n256_d32_h1_g2_grid_causal_f32")
+    seq, dim, heads, gpus, seed, causal, tile, prec = (int(x) for x in g["meta"])
+    qn, kn, vn, dn, scale = orc.generate_inputs(seq, dim, heads, 1, seed, np.float32)
+    to = lambda a: torch.from_numpy(np.ascontiguousarray(a.transpose(1, 0, 2)[None])).cuda()
+    spec = {"n_query_blocks": int(g["grid"][0]), "n_key_blocks": int(g["grid"][1]),
+            "skip": g["grid_skip"].tolist(), "causal": True}
+    poison_allocator()
+    res = run_ring_pass(to(qn), to(kn), to(vn), gpus, dout=to(dn), mask=spec, zigzag=False)
+    torch.cuda.synchronize()
+    for key, got in (("o", res.out), ("dq", res.dq), ("dk", res.dk), ("dv", res.dv)):
+        assert rel_err(got, g[key].transpose(1, 0, 2)[None]) < 1e-5, key
+
+
 def test_c1_golden_fp32(golden):
     """BASELINE configs[0] (seq 1024, d 64, 2 heads, G 2, fp32) against the
     reference's own outputs (tests/golden, produced by the reference)."""

@@ -301,3 +301,63 @@ def test_qtravel_ledger_counts_fewer_elements(causal, zigzag):
                     if not plan_hop((r - h) % G, G, (-h) % G, n, causal, zigzag).skip)
         # Q, dO (n*H*D each), lse + D (H*n each) per rotation; one dQ part per visited block
         assert led.elements_sent_backward == (G - 1) * (2 * n * H * D + 2 * H * n) + parts * n * H * D
+
+
+# ---------------------------------------------------------------- block-sparse grid masks (f3)
+
+GRID_GOLDENS = [("ring_n64_d16_h2_g4_grid_f64", False, "kv"),
+                ("ring_n128_d16_h1_g4_grid_causal_f64", False, "kv"),
+                ("ring_n128_d16_h1_g4_grid_causal_f64", True, "kv"),
+                ("ring_n128_d16_h1_g4_grid_causal_f64", True, "q")]
+
+
+@pytest.mark.parametrize("name,zigzag,payload", GRID_GOLDENS)
+def test_engine_grid_mask_matches_reference_golden(golden, name, zigzag, payload):
+    """BlockGrid masks (masking.py:33-147) through the whole ring engine, against the
+    reference's own outputs (tests/golden, made by running the reference)."""
+    from paper_2403_09347_b200 import run_ring_pass
+    g = golden(name)
+    seq, dim, heads, gpus, seed, causal, tile, prec = (int(x) for x in g["meta"])
+    q, k, v, do, scale = orc.generate_inputs(seq, dim, heads, 1, seed, np.float64)
+    to = lambda a: torch.from_numpy(np.ascontiguousarray(a.transpose(1, 0, 2)[None]))
+    spec = {"n_query_blocks": int(g["grid"][0]), "n_key_blocks": int(g["grid"][1]),
+            "skip": g["grid_skip"].tolist(), "causal": bool(causal)}
+    res = run_ring_pass(to(q), to(k), to(v), gpus, dout=to(do), zigzag=zigzag,
+                        kernels=OracleKernels(), mask=spec, bwd_payload=payload)
+    # lse is fp32 by contract, so gradients carry its rounding (same bar as
+    # test_engine_loopback_matches_dense)
+    for key, got, tol in (("o", res.out, 1e-10), ("dq", res.dq, 1e-5), ("dk", res.dk, 1e-5),
+                          ("dv", res.dv, 1e-5)):
+        ref = g[key].transpose(1, 0, 2)[None]
+        assert np.max(np.abs(got.numpy() - ref)) < tol, key
+    assert np.max(np.abs(res.lse.numpy() - g["lse"][None])) < 1e-5
+
+
+def test_grid_mask_validation_and_hop_skip():
+    from paper_2403_09347_b200 import MaskError
+    from paper_2403_09347_b200.masks import GridMask
+    from paper_2403_09347_b200.schedule import plan_hop
+    g = GridMask(4, 4, frozenset({(0, 0), (0, 1), (0, 2), (0, 3)})).bind(64)
+    with pytest.raises(MaskError):              # query block 0 sees no key
+        g.validate(causal=False)
+    with pytest.raises(MaskError):
+        GridMask(3, 4).bind(64)                  # 3 does not divide 64
+    with pytest.raises(MaskError):
+        GridMask(2, 2, frozenset({(2, 0)}))      # cell outside the grid
+    with pytest.raises(MaskError):               # causal: row 0 only sees key 0
+        GridMask(2, 2, frozenset({(0, 0)})).bind(8).validate(causal=True)
+    # a hop whose whole rectangle is skipped becomes SKIP (BlockMask.decision)
+    g = GridMask(4, 4, frozenset({(1, 3)})).bind(64)
+    assert plan_hop(1, 4, 2, 16, False, False, None, g).skip      # queries 16-31 x keys 48-63
+    p = plan_hop(1, 4, 1, 16, False, False, None, g)
+    assert not p.skip and p.grid is g
+
+
+def test_grid_mask_from_spec_file(tmp_path):
+    from paper_2403_09347_b200.masks import GridMask
+    path = tmp_path / "mask.json"
+    path.write_text('{"n_query_blocks": 2, "n_key_blocks": 4, "skip": [[1, 0]], "causal": true}')
+    g, causal = GridMask.from_spec(str(path))
+    assert causal and g.n_query_blocks == 2 and g.skip == frozenset({(1, 0)})
+    assert GridMask.from_spec("causal") == (None, True)
+    assert GridMask.from_spec(None) == (None, False)

@@ -45,6 +45,9 @@ def test_finalize_hand_value_and_unvisited_rows():
     ("ring_n64_d16_h2_g4_f64", 1e-12),
     ("ring_n64_d16_h1_g4_causal_f64", 1e-12),
     ("ring_n256_d64_h1_g2_causal_f32", 2e-6),
+    ("ring_n64_d16_h2_g4_grid_f64", 1e-12),
+    ("ring_n128_d16_h1_g4_grid_causal_f64", 1e-12),
+    ("ring_n256_d32_h1_g2_grid_causal_f32", 2e-6),
 ])
 def test_oracle_ring_matches_reference(golden, name, tol):
     g = golden(name)
@@ -55,9 +58,12 @@ def test_oracle_ring_matches_reference(golden, name, tol):
     cs = np.array([float(np.sum(a.astype(np.float64))) for a in (q, k, v, do)] +
                   [float(a.reshape(-1)[7]) for a in (q, k, v, do)])
     assert np.array_equal(cs, g["input_checksum"])
+    grid = None
+    if "grid" in g:   # block-sparse grid mask (BlockGrid, masking.py:33-63)
+        grid = orc.GridCells(g["grid"][0], g["grid"][1], g["grid_skip"].tolist(), seq)
     for s in range(heads):
         dq, dk, dv, o, lse = orc.ring_backward(q[s], k[s], v[s], do[s], scale, gpus,
-                                               causal=bool(causal), tile=tile)
+                                               causal=bool(causal), tile=tile, grid=grid)
         for key, got in (("o", o), ("lse", lse), ("dq", dq), ("dk", dk), ("dv", dv)):
             ref = g[key][s]
             err = np.max(np.abs(got.astype(np.float64) - ref)) / max(np.max(np.abs(ref)), 1e-30)
