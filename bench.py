@@ -241,7 +241,7 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     def step(qq, kk, vv, dd, recorders=None):
         o, lse = burst_attn_func(qq, kk, vv, causal=causal, zigzag=zigzag, _kernels=kern,
-                                 _recorders=recorders)
+                                 comm=args.comm, _recorders=recorders)
         grads = torch.autograd.grad(o, (qq, kk, vv), dd)
         return o, grads
 
@@ -391,7 +391,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         "data": "synthetic (seeded N(0,1) q/k/v/dO)",
         "config": {"workload": cfg["workload"], "seq": N, "heads": H, "head_dim": D, "batch": B,
                    "causal": causal, "partition": "zigzag" if zigzag else "contiguous",
-                   "parallelism": f"ring sp{world}", "l2": "inputs larger than L2 "
+                   "parallelism": f"ring sp{world}", "comm": args.comm if world > 1 else None,
+                   "l2": "inputs larger than L2 "
                    f"({tensor_bytes / 2**30:.2f} GiB per tensor per rank)"},
         "tflops_per_gpu": tflops_gpu, "tc_peak_frac": tflops_gpu / peak_sus,
         "tc_peak_frac_of_burst": tflops_gpu / peak_burst,
@@ -413,6 +414,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-rows", type=int, default=512)
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "ce"],
+                    help="ring transport at N>1: NCCL send/recv, or copy engines over CUDA IPC")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))

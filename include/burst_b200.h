@@ -17,6 +17,8 @@
  *   burst_bwd_finalize   sim._collect gradient assembly    (sim.py:450-471)
  *   burst_tl_sum         same, for travelling-query dQ contributions (ring.py:65-83)
  *   burst_ring_*         sim.RingChannel send/recv, DoubleBuffer (sim.py:281-332)
+ *   burst_ipc_*, burst_copy_async, burst_event_* / burst_stream_wait_event
+ *                        the same hand-off over copy engines (zero SM), SURVEY f1
  *
  * Tensor layouts (row-major, contiguous):
  *   q, k, v, o, dout, dq, dk, dv : [batch, n, heads, head_dim]  (bf16 or f32)
@@ -146,6 +148,25 @@ typedef struct {
 } burst_p2p;
 BURST_API int burst_ring_sendrecv(void* ring, const burst_p2p* ops, int nops, void* stream);
 BURST_API int burst_ring_destroy(void* ring);
+
+/* Zero-SM ring transport (copy engines + CUDA IPC, ring.IpcTransport): the CUDA
+ * runtime pieces of a mailbox exchange.  Handles are opaque byte blobs of
+ * burst_ipc_handle_bytes() bytes (mem and event handles have the same size). */
+BURST_API size_t burst_ipc_handle_bytes(void);
+/* Dedicated device allocation for a mailbox (an IPC handle names a whole allocation). */
+BURST_API int burst_ipc_alloc(size_t bytes, void** dev_ptr);
+BURST_API int burst_ipc_free(void* dev_ptr);
+BURST_API int burst_ipc_mem_handle(void* dev_ptr, void* out_handle);
+BURST_API int burst_ipc_open_mem(const void* handle, void** dev_ptr);
+BURST_API int burst_ipc_close_mem(void* dev_ptr);
+/* Interprocess event (timing disabled); its handle opens in another process. */
+BURST_API int burst_ipc_event_create(void** event, void* out_handle);
+BURST_API int burst_ipc_event_open(const void* handle, void** event);
+BURST_API int burst_event_record(void* event, void* stream);
+BURST_API int burst_stream_wait_event(void* stream, void* event);
+BURST_API int burst_event_destroy(void* event);
+/* Device-to-device (or peer) copy on `stream`, executed by the copy engines. */
+BURST_API int burst_copy_async(void* dst, const void* src, size_t bytes, void* stream);
 
 BURST_API const char* burst_last_error(void);
 BURST_API int burst_version(void);

@@ -62,6 +62,18 @@ _SIGS = {
     "burst_tl_sum": ([_c_i32, _c_i32, _c_i32, _c_i32, _c_i64, ctypes.POINTER(_c_p), _c_i32, _c_p,
                       _c_p], _c_i32),
     "burst_read_flags": ([_c_p, ctypes.POINTER(_c_i32)], _c_i32),
+    "burst_ipc_handle_bytes": ([], _c_sz),
+    "burst_ipc_alloc": ([_c_sz, ctypes.POINTER(_c_p)], _c_i32),
+    "burst_ipc_free": ([_c_p], _c_i32),
+    "burst_ipc_mem_handle": ([_c_p, _c_p], _c_i32),
+    "burst_ipc_open_mem": ([_c_p, ctypes.POINTER(_c_p)], _c_i32),
+    "burst_ipc_close_mem": ([_c_p], _c_i32),
+    "burst_ipc_event_create": ([ctypes.POINTER(_c_p), _c_p], _c_i32),
+    "burst_ipc_event_open": ([_c_p, ctypes.POINTER(_c_p)], _c_i32),
+    "burst_event_record": ([_c_p, _c_p], _c_i32),
+    "burst_stream_wait_event": ([_c_p, _c_p], _c_i32),
+    "burst_event_destroy": ([_c_p], _c_i32),
+    "burst_copy_async": ([_c_p, _c_p, _c_sz, _c_p], _c_i32),
     "burst_ring_unique_id": ([_c_p], _c_i32),
     "burst_ring_create": ([_c_p, _c_i32, _c_i32, _c_i32, ctypes.POINTER(_c_p)], _c_i32),
     "burst_ring_exchange": ([_c_p, _c_p, _c_p, _c_sz, _c_i32, _c_i32, _c_p], _c_i32),

@@ -20,8 +20,8 @@ import torch
 from .errors import ConfigError, ShapeError
 from .masks import GridMask
 from .kernels import CudaKernels, check_qkv, default_scale
-from .ring import (NcclTransport, SoloTransport, ring_backward, ring_backward_qtravel,
-                   ring_forward, run_ranks)
+from .ring import (IpcTransport, NcclTransport, SoloTransport, ring_backward,
+                   ring_backward_qtravel, ring_forward, run_ranks)
 from .schedule import shard, unshard
 from .trace import PassRecorder, PassTrace, merge
 
@@ -36,16 +36,20 @@ def _default_kernels():
     return _kernels
 
 
-def _transport_for(group):
+def _transport_for(group, comm: str = "nccl"):
+    """Ring transport of `group`: "nccl" (NCCL send/recv kernels) or "ce" (zero-SM
+    copy-engine pushes into CUDA-IPC mailboxes, ring.IpcTransport)."""
     import torch.distributed as dist
     if group is None and not (dist.is_available() and dist.is_initialized()):
         return SoloTransport()
     world = dist.get_world_size(group)
     if world == 1:
         return SoloTransport()
-    key = (id(group), torch.cuda.current_device())
+    if comm not in ("nccl", "ce"):
+        raise ConfigError(f"comm must be 'nccl' or 'ce', got {comm!r}")
+    key = (id(group), torch.cuda.current_device(), comm)
     if key not in _transports:
-        _transports[key] = NcclTransport(group)
+        _transports[key] = NcclTransport(group) if comm == "nccl" else IpcTransport(group)
     return _transports[key]
 
 
@@ -73,8 +77,8 @@ class _BurstAttnFn(torch.autograd.Function):
 
 def burst_attn_func(q, k, v, causal: bool = False, softmax_scale: float | None = None,
                     group=None, zigzag: bool | None = None, valid_len: int | None = None, *,
-                    bwd_payload: str = "kv", mask=None, _transport=None, _kernels=None,
-                    _recorders=None):
+                    bwd_payload: str = "kv", mask=None, comm: str = "nccl", _transport=None,
+                    _kernels=None, _recorders=None):
     """BurstAttention over the ranks of `group` (NCCL ring over NVLink).
 
     q, k, v: [batch, n_local, heads, head_dim] shards of the global sequence
@@ -90,6 +94,7 @@ def burst_attn_func(q, k, v, causal: bool = False, softmax_scale: float | None =
     `mask`: block-sparse grid over the GLOBAL score matrix -- a masks.GridMask or a
     mask_from_spec value (dict / JSON path with n_query_blocks, n_key_blocks, skip and
     an optional causal flag; masking.py:150-180); composes with `causal`.
+    `comm`: ring transport, "nccl" (default) or "ce" (copy engines + CUDA IPC, no SM).
     `_recorders`: optional (forward, backward) trace.PassRecorder pair that
     records this rank's measured hop timeline and byte ledger.
     """
@@ -99,7 +104,7 @@ def burst_attn_func(q, k, v, causal: bool = False, softmax_scale: float | None =
     scale = default_scale(q.shape[-1]) if softmax_scale is None else float(softmax_scale)
     if not scale > 0:
         raise ShapeError(f"scale must be finite and positive, got {scale}")
-    transport = _transport if _transport is not None else _transport_for(group)
+    transport = _transport if _transport is not None else _transport_for(group, comm)
     kernels = _kernels if _kernels is not None else _default_kernels()
     if zigzag is None:
         zigzag = bool(causal) and transport.world > 1

@@ -19,7 +19,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libburst_b200.so")
-SOURCES = ["capi.cu", "ring_nccl.cu"]
+SOURCES = ["capi.cu", "ring_nccl.cu", "ring_ipc.cu"]
 HEADERS = ["ptx.cuh", "common.cuh", "lao_fwd_sm100.cuh", "lao_bwd_sm100.cuh", "lao_bwd2_sm100.cuh",
            "lao_bwd3_sm100.cuh", "lao_bwd4_sm100.cuh", "lao_bwd5_sm100.cuh",
            "simt_f32.cuh",

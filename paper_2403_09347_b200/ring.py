@@ -20,6 +20,7 @@ Transports:
   NcclTransport        one NCCL communicator via the C ABI (burst_ring_*); GPU
   LoopbackTransport    G ranks as threads in one process (the reference's
                        threaded executor); single-GPU simulation of a ring
+  IpcTransport         copy-engine pushes into CUDA-IPC mailboxes (zero SM, f1)
   TorchDistTransport   torch.distributed P2P (gloo on CPU for host-logic tests)
 """
 
@@ -134,6 +135,149 @@ class NcclTransport:
         if getattr(self, "handle", None):
             _lib.load().burst_ring_destroy(self.handle)
             self.handle = None
+
+
+class IpcTransport:
+    """Zero-SM transport: each send is a copy-engine
+    cudaMemcpyAsync into the receiver's CUDA-IPC mailbox (NVLink for peers on other
+    GPUs), ordered by interprocess CUDA events; no SM is used, so the transfers
+    never compete with the full-grid LAO kernels the way NCCL send/recv kernels do.
+
+    Per exchange (all ranks call it in lockstep, like the reference's rounds,
+    sim.py:551-574), with mailbox slot s alternating 0/1 (the DoubleBuffer of
+    sim.py:316-332):
+      1. capacity: every rank announces the bytes it will receive from each peer;
+         a mailbox too small is reallocated and its IPC handle re-shared
+         (all_gather_object; also the barrier that orders step 2 after the
+         receivers' step-4 records of two exchanges ago);
+      2. sender: comm stream waits the receiver's consumed[s] event, copies its
+         SEND tensors back to back into the receiver's mailbox[from me][s], then
+         records its own ready[s];
+      3. barrier (every ready[s] recorded before anyone waits on it);
+      4. receiver: waits the sender's ready[s], copies mailbox -> RECV tensors in
+         the same order, records consumed[s].
+    Host-side handshakes use `group` (gloo is enough).
+    """
+
+    def __init__(self, group=None, device: torch.device | None = None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        lib = _lib.load()
+        self.hbytes = int(lib.burst_ipc_handle_bytes())
+        self.slot = 0
+        self.boxes = {}          # (src, slot) -> (device pointer, capacity): my mailboxes
+        self.peer_box = {}       # (dst, slot) -> (device pointer, capacity) in dst's memory
+        self.ready, self.consumed = [], []
+        handles = []
+        for _ in range(2):
+            for lst in (self.ready, self.consumed):
+                ev, h = ctypes.c_void_p(), (ctypes.c_char * self.hbytes)()
+                _lib.call("burst_ipc_event_create", ctypes.byref(ev), h)
+                lst.append(ev)
+                handles.append(bytes(h))
+        allh = [None] * self.world
+        dist.all_gather_object(allh, handles, group=group)
+        self.peer_ready, self.peer_consumed = {}, {}
+        for r, hs in enumerate(allh):
+            if r == self.rank:
+                continue
+            for s in range(2):
+                for key, idx in ((self.peer_ready, 2 * s), (self.peer_consumed, 2 * s + 1)):
+                    ev = ctypes.c_void_p()
+                    buf = (ctypes.c_char * self.hbytes).from_buffer_copy(hs[idx])
+                    _lib.call("burst_ipc_event_open", buf, ctypes.byref(ev))
+                    key[(r, s)] = ev
+        self.started = set()     # slots whose consumed event has been recorded once
+        self.retired = []        # outgrown mailboxes (freed in close())
+
+    def _grow(self, needs: dict, s: int) -> dict:
+        """Reallocate my mailboxes that are too small; return {src: handle bytes}."""
+        out = {}
+        for src, nbytes in needs.items():
+            box = self.boxes.get((src, s))
+            if box is None or box[1] < nbytes:
+                cap = max(nbytes, 2 * box[1] if box is not None else 0)
+                if box is not None:   # the peer may still map it: freed in close()
+                    self.retired.append(box[0])
+                ptr = ctypes.c_void_p()
+                _lib.call("burst_ipc_alloc", cap, ctypes.byref(ptr))
+                self.boxes[(src, s)] = (ptr.value, cap)
+                h = (ctypes.c_char * self.hbytes)()
+                _lib.call("burst_ipc_mem_handle", ptr, h)
+                out[src] = (bytes(h), cap)
+        return out
+
+    def sendrecv(self, ops, stream):
+        d, s = self.dist, self.slot
+        self.slot ^= 1
+        sh = ctypes.c_void_p(stream.cuda_stream)
+        needs = defaultdict(int)
+        for kind, t, peer in ops:
+            if kind == RECV:
+                needs[peer] += t.numel() * t.element_size()
+        # 1. capacity / handle exchange (+ the barrier of the protocol)
+        new = self._grow(needs, s)
+        allnew = [None] * self.world
+        d.all_gather_object(allnew, new, group=self.group)
+        for r, m in enumerate(allnew):
+            if r != self.rank and self.rank in m:
+                h, cap = m[self.rank]
+                old = self.peer_box.get((r, s))
+                if old is not None:
+                    _lib.call("burst_ipc_close_mem", ctypes.c_void_p(old[0]))
+                ptr = ctypes.c_void_p()
+                buf = (ctypes.c_char * self.hbytes).from_buffer_copy(h)
+                _lib.call("burst_ipc_open_mem", buf, ctypes.byref(ptr))
+                self.peer_box[(r, s)] = (ptr.value, cap)
+        # 2. pushes into the receivers' mailboxes (copy engines)
+        offs = defaultdict(int)
+        waited = set()
+        for kind, t, peer in ops:
+            if kind != SEND:
+                continue
+            if s in self.started and peer not in waited:
+                _lib.call("burst_stream_wait_event", sh, self.peer_consumed[(peer, s)])
+                waited.add(peer)
+            ptr, cap = self.peer_box[(peer, s)]
+            nb = t.numel() * t.element_size()
+            if offs[peer] + nb > cap:
+                raise RingDesyncError(f"rank {self.rank}: payload to {peer} exceeds its mailbox")
+            _lib.call("burst_copy_async", ctypes.c_void_p(ptr + offs[peer]),
+                      ctypes.c_void_p(t.data_ptr()), nb, sh)
+            offs[peer] += nb
+        _lib.call("burst_event_record", self.ready[s], sh)
+        # 3. every ready[s] recorded before anyone waits on it
+        d.barrier(group=self.group)
+        # 4. mailbox -> destination tensors
+        offs = defaultdict(int)
+        waited = set()
+        for kind, t, peer in ops:
+            if kind != RECV:
+                continue
+            if peer not in waited:
+                _lib.call("burst_stream_wait_event", sh, self.peer_ready[(peer, s)])
+                waited.add(peer)
+            box = self.boxes[(peer, s)][0]
+            nb = t.numel() * t.element_size()
+            _lib.call("burst_copy_async", ctypes.c_void_p(t.data_ptr()),
+                      ctypes.c_void_p(box + offs[peer]), nb, sh)
+            offs[peer] += nb
+        _lib.call("burst_event_record", self.consumed[s], sh)
+        self.started.add(s)
+
+    def close(self):
+        lib = _lib.load()
+        torch.cuda.synchronize(self.device)
+        for ptr, _ in self.peer_box.values():
+            lib.burst_ipc_close_mem(ctypes.c_void_p(ptr))
+        self.peer_box = {}
+        self.dist.barrier(group=self.group)     # every peer unmapped before freeing
+        for ptr in [p for p, _ in self.boxes.values()] + self.retired:
+            lib.burst_ipc_free(ctypes.c_void_p(ptr))
+        self.boxes, self.retired = {}, []
 
 
 class TorchDistTransport:
