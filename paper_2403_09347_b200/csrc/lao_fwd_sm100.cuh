@@ -81,7 +81,10 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
   const int lane = threadIdx.x & 31;
   const int b = blockIdx.z, h = blockIdx.y;
   const int64_t q_end = hp.q_begin + hp.q_len;
-  const int64_t row0 = hp.q_begin + (int64_t)blockIdx.x * (2 * BM);
+  // causal: later query rows see more keys, so launch them first (longest-first
+  // order shortens the tail wave of the grid)
+  const int64_t xb = hp.causal ? (int64_t)(gridDim.x - 1 - blockIdx.x) : (int64_t)blockIdx.x;
+  const int64_t row0 = hp.q_begin + xb * (2 * BM);
 
   // Key span this CTA needs: causal => a prefix of the hop's keys (monotone maps).
   int64_t kspan = hp.k_len;
