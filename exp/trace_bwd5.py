@@ -19,8 +19,9 @@ _lib.load().burst_exp_trace_read(buf)
 t = np.array(buf, dtype=np.int64).reshape(2, 16, 64)
 names = {3: "sm:s_full", 4: "sm:p_arrive", 0: "mma:p_full", 11: "mma:S^T+1", 5: "sm:dp_full",
          6: "sm:ds_arrive", 1: "mma:dK", 12: "mma:dQ", 7: "dq:dq_full", 8: "dq:arrive",
-         2: "mma:dq_empty", 10: "mma:dOA+1", 9: "dq:issued"}
-order = [3, 4, 0, 11, 5, 6, 1, 12, 7, 8, 2, 10, 9]
+         2: "mma:dq_empty", 10: "mma:dOA+1", 9: "dq:issued", 13: "d:ld_done", 14: "d:bar_done",
+         15: "d:st_done"}
+order = [3, 4, 0, 11, 5, 13, 14, 15, 6, 1, 12, 7, 8, 2, 10, 9]
 for c in range(2):
     base = t[c, 3, 0]
     print(f"CTA {c} (0 = leader)")

@@ -127,6 +127,11 @@ BURST_API int burst_bwd_finalize(int dtype, int batch, int heads, int head_dim, 
 BURST_API int burst_tl_sum(int dtype, int batch, int heads, int head_dim, int64_t n,
                  const float* const* parts, int nparts, void* out, void* stream);
 
+/* Select the bf16 head_dim-128 backward kernel for later burst_lao_bwd calls:
+ * 0 = default (BURST_BWD_KERNEL env or 4), 1 = lao_bwd, 3 = bwd3, 4 = bwd4 (default),
+ * 5 (or 2) = bwd5 (CTA pair, dS^T in TMEM).  Process-wide. */
+BURST_API int burst_set_bwd_variant(int variant);
+
 /* Non-zero device-side flags raised by kernels since the last call (bit 0: a
  * row with no visible key, bit 1: non-finite output).  Synchronises `stream`. */
 BURST_API int burst_read_flags(void* stream, int* flags_out);

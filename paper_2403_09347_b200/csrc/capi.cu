@@ -7,12 +7,12 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
 
 #include "../../include/burst_b200.h"
 #include "aux_kernels.cuh"
-#include "lao_bwd2_sm100.cuh"
 #include "lao_bwd3_sm100.cuh"
 #include "lao_bwd4_sm100.cuh"
 #include "lao_bwd5_sm100.cuh"
@@ -223,36 +223,6 @@ int launch_bwd_bf16(const burst_hop* h, const void* q, const void* k, const void
   return BURST_OK;
 }
 
-// CTA-pair backward (cta_group::2, 256 keys per pair): half the dQ reduction volume.
-int launch_bwd2_bf16(const burst_hop* h, const void* q, const void* k, const void* v, const void* dout,
-                     const float* stats, float* dq_acc, float* dk, float* dv, int acc, cudaStream_t st) {
-  bwd2::Params p;
-  memset(&p, 0, sizeof(p));
-  int rc;
-  if ((rc = make_tmap(&p.tm_q128, q, h->n_q, h->heads, 128, h->batch))) return rc;
-  if ((rc = make_tmap(&p.tm_q64, q, h->n_q, h->heads, 128, h->batch, 64))) return rc;
-  if ((rc = make_tmap(&p.tm_do128, dout, h->n_q, h->heads, 128, h->batch))) return rc;
-  if ((rc = make_tmap(&p.tm_do64, dout, h->n_q, h->heads, 128, h->batch, 64))) return rc;
-  if ((rc = make_tmap(&p.tm_k, k, h->n_k, h->heads, 128, h->batch))) return rc;
-  if ((rc = make_tmap(&p.tm_v, v, h->n_k, h->heads, 128, h->batch))) return rc;
-  p.stats = stats; p.dq_acc = dq_acc; p.dk_acc = dk; p.dv_acc = dv;
-  p.hop = *h;
-  p.scale_log2 = h->softmax_scale * kLog2e;
-  p.scale = h->softmax_scale;
-  p.accumulate = acc;
-#ifdef BURST_TRACE
-  p.trace = trace_buffer();
-#endif
-  static std::once_flag once;
-  static int attr_rc = 0;
-  std::call_once(once, [] { attr_rc = set_smem(bwd2::lao_bwd2_kernel, bwd2::kSmemBytes); });
-  if (attr_rc) return attr_rc;
-  dim3 grid((unsigned)(2 * ceil_div(h->k_len, 2 * bwd2::BN)), h->heads, h->batch);
-  bwd2::lao_bwd2_kernel<<<grid, bwd2::kThreads, bwd2::kSmemBytes, st>>>(p);
-  CHECK_LAUNCH();
-  return BURST_OK;
-}
-
 // CTA-pair backward with two P/dS warpgroups and SMEM-staged dQ reduction (variant 5).
 int launch_bwd5_bf16(const burst_hop* h, const void* q, const void* k, const void* v, const void* dout,
                      const float* stats, float* dq_acc, float* dk, float* dv, int acc, cudaStream_t st) {
@@ -285,15 +255,18 @@ int launch_bwd5_bf16(const burst_hop* h, const void* q, const void* k, const voi
 }
 
 // Backward kernel variant for bf16 (BURST_BWD_KERNEL: 1 = single CTA + red.global,
-// 2 = CTA pair, 3 = single CTA + SMEM-staged TMA bulk reductions, 4 = variant 3 with two
+// 2 = alias of 5, 3 = single CTA + SMEM-staged TMA bulk reductions, 4 = variant 3 with two
 // P/dS warpgroups and a double-buffered dQ drain, 5 = CTA pair with two P/dS warpgroups,
 // dS^T in TMEM and SMEM-staged dQ reduction; default 4).
+std::atomic<int> g_bwd_override{0};   // burst_set_bwd_variant (0 = env / default)
+
 int bwd_variant() {
   static int v = [] {
     const char* e = getenv("BURST_BWD_KERNEL");
     return (e && e[0] >= '1' && e[0] <= '5') ? e[0] - '0' : 4;
   }();
-  return v;
+  const int o = g_bwd_override.load(std::memory_order_relaxed);
+  return o ? o : v;
 }
 
 template <int D>
@@ -489,10 +462,10 @@ int burst_lao_bwd(const burst_hop* hop, const void* q, const void* k, const void
     // the staged kernel reduces whole 128-row TL tiles: needs 128-aligned query ranges
     const int var = (bwd_variant() >= 3 && hop->q_begin % 128 != 0) ? 1 : bwd_variant();
     if (hop->head_dim == 128) {
-      if (var == 2) return launch_bwd2_bf16(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
       if (var == 3) return launch_bwd3_bf16<128>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
       if (var == 4) return launch_bwd4_bf16<128>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
-      if (var == 5) return launch_bwd5_bf16(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
+      if (var == 2 || var == 5)   // 2: the first pair kernel, superseded by bwd5
+        return launch_bwd5_bf16(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
       return launch_bwd_bf16<128>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
     }
     if (var == 3) return launch_bwd3_bf16<64>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
@@ -550,6 +523,12 @@ int burst_tl_sum(int dtype, int batch, int heads, int head_dim, int64_t n, const
     aux::tl_sum_kernel<float><<<grid_for(work, 256), 256, 0, st>>>(batch, heads, head_dim, n, pp,
                                                                   nparts, (float*)out);
   CHECK_LAUNCH();
+  return BURST_OK;
+}
+
+int burst_set_bwd_variant(int variant) {
+  if (variant < 0 || variant > 5) return fail(BURST_E_SHAPE, "backward variant must be 0 (default) .. 5");
+  g_bwd_override.store(variant, std::memory_order_relaxed);
   return BURST_OK;
 }
 

@@ -401,8 +401,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       ptx::tmem_ld32(tbase + lane_off + kDP + 64 * hq + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
       ptx::tmem_wait_ld();
       ptx::reg_fence(r);
+      if (hq == 0) BTRACE5(13, i);
       ptx::tc_fence_before();
       ptx::named_bar_sync(2, 2 * BN);            // every dP^T column read before dS^T lands
+      if (hq == 0) BTRACE5(14, i);
       ptx::mbar_wait(bar + B_DSQE, (i & 1) ^ 1);  // dQ_{i-1} retired: DSQ / XS free
       if (local && t == 0) ptx::mbar_expect_tx(bar + B_X, 16384);   // the peer's half of this tile
       ptx::tc_fence_after();
@@ -423,6 +425,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         *reinterpret_cast<uint4*>(dst_row + ((ch ^ (dsq_row & 7)) << 4)) =
             make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
       ptx::tmem_wait_st();
+      if (hq == 0) BTRACE5(15, i);
       ptx::fence_proxy_async_smem();
       if (!local) {
         ptx::named_bar_sync(3, BN);

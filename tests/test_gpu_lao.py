@@ -236,3 +236,27 @@ def test_bf16_padding(N, world, causal):
     assert max_abs(res.out, o) < BF16_TOL and max_abs(res.lse, lse) < 1e-2
     for got, ref in ((res.dq, dq), (res.dk, dk), (res.dv, dv)):
         assert max_abs(got, ref) < BF16_TOL
+
+
+@pytest.fixture
+def bwd_variant():
+    """Select a backward kernel variant for one test (burst_set_bwd_variant)."""
+    from paper_2403_09347_b200 import _lib
+    yield lambda v: _lib.call("burst_set_bwd_variant", v)
+    _lib.call("burst_set_bwd_variant", 0)
+
+
+@pytest.mark.parametrize("variant", [1, 3, 5])
+@pytest.mark.parametrize("world,causal,zigzag", [(1, False, False), (2, True, True),
+                                                 (4, False, False)])
+def test_backward_variants_parity(bwd_variant, variant, world, causal, zigzag):
+    """The non-default bf16 backward kernels (lao_bwd, bwd3, the CTA-pair bwd5) against
+    the oracle on the same rings as the default."""
+    bwd_variant(variant)
+    N = 512 * world if world > 1 else 1024
+    q, k, v, do = make_inputs(1, N, 2, 128, seed=variant * 10 + world)
+    poison_allocator()
+    res = _run(q, k, v, do, world, causal, zigzag)
+    o, lse, dq, dk, dv = oracle_ring(q, k, v, do, world, causal, zigzag)
+    for name, got, ref in (("dq", res.dq, dq), ("dk", res.dk, dk), ("dv", res.dv, dv)):
+        assert max_abs(got, ref) < BF16_TOL, name
