@@ -169,6 +169,9 @@ int launch_fwd_bf16(const burst_hop* h, const void* q, const void* k, const void
   p.hop = *h;
   p.scale_log2 = h->softmax_scale * kLog2e;
   p.first_hop = first; p.finalize = fin;
+#ifdef BURST_TRACE
+  p.trace = trace_buffer();
+#endif
   static std::once_flag once;
   static int attr_rc = 0;
   std::call_once(once, [] { attr_rc = set_smem(fwd::lao_fwd_kernel<D>, fwd::Cfg<D>::kSmemBytes); });

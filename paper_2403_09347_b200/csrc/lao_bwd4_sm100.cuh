@@ -368,10 +368,15 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
         for (int c4 = 0; c4 < 16; ++c4) {
           const float4 L = lse4[c4];
           // masked entries are zeroed below, so the FMA-pipe exp2 is safe everywhere here
-          pr[4 * c4 + 0] = ptx::ex2_mixed(fmaf(__uint_as_float(r[4 * c4 + 0]), c2, -L.x), 4 * c4 + 0);
-          pr[4 * c4 + 1] = ptx::ex2_mixed(fmaf(__uint_as_float(r[4 * c4 + 1]), c2, -L.y), 4 * c4 + 1);
-          pr[4 * c4 + 2] = ptx::ex2_mixed(fmaf(__uint_as_float(r[4 * c4 + 2]), c2, -L.z), 4 * c4 + 2);
-          pr[4 * c4 + 3] = ptx::ex2_mixed(fmaf(__uint_as_float(r[4 * c4 + 3]), c2, -L.w), 4 * c4 + 3);
+          // x = S * scale*log2e - lse*log2e on packed fp32x2 (FFMA2)
+          const float2 xa = ptx::ffma2(make_float2(__uint_as_float(r[4 * c4 + 0]), __uint_as_float(r[4 * c4 + 1])),
+                                       make_float2(c2, c2), make_float2(-L.x, -L.y));
+          const float2 xb = ptx::ffma2(make_float2(__uint_as_float(r[4 * c4 + 2]), __uint_as_float(r[4 * c4 + 3])),
+                                       make_float2(c2, c2), make_float2(-L.z, -L.w));
+          pr[4 * c4 + 0] = ptx::ex2(xa.x);
+          pr[4 * c4 + 1] = ptx::ex2(xa.y);
+          pr[4 * c4 + 2] = ptx::ex2(xb.x);
+          pr[4 * c4 + 3] = ptx::ex2(xb.y);
         }
       }
       if (!warp_full) {
@@ -407,10 +412,15 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
         for (int j4 = 0; j4 < 8; ++j4) {
           const float4 Dv = dst4[qc * 8 + j4];
           const int c = qc * 32 + 4 * j4;
-          pk[2 * j4] = ptx::pack_bf16(pr[c] * (__uint_as_float(r[4 * j4]) - Dv.x),
-                                      pr[c + 1] * (__uint_as_float(r[4 * j4 + 1]) - Dv.y));
-          pk[2 * j4 + 1] = ptx::pack_bf16(pr[c + 2] * (__uint_as_float(r[4 * j4 + 2]) - Dv.z),
-                                          pr[c + 3] * (__uint_as_float(r[4 * j4 + 3]) - Dv.w));
+          // dS = P * (dP - D) on packed fp32x2 (FADD2 + FMUL2)
+          const float2 da = ptx::fmul2(make_float2(pr[c], pr[c + 1]),
+                                       ptx::fadd2(make_float2(__uint_as_float(r[4 * j4]), __uint_as_float(r[4 * j4 + 1])),
+                                                  make_float2(-Dv.x, -Dv.y)));
+          const float2 db = ptx::fmul2(make_float2(pr[c + 2], pr[c + 3]),
+                                       ptx::fadd2(make_float2(__uint_as_float(r[4 * j4 + 2]), __uint_as_float(r[4 * j4 + 3])),
+                                                  make_float2(-Dv.z, -Dv.w)));
+          pk[2 * j4] = ptx::pack_bf16(da.x, da.y);
+          pk[2 * j4 + 1] = ptx::pack_bf16(db.x, db.y);
         }
 #ifdef BURST_EXP_NO_DS_STS   // experiment: dS never reaches SMEM (wrong results)
         if (pk[0] == 0x7f7f7f7fu)

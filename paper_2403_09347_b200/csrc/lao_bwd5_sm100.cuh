@@ -371,10 +371,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int c4 = 0; c4 < 16; ++c4) {
           const float4 Lv = lse4[c4];
-          pr[4 * c4 + 0] = ptx::ex2(fmaf(__uint_as_float(r[4 * c4 + 0]), c2, -Lv.x));
-          pr[4 * c4 + 1] = ptx::ex2(fmaf(__uint_as_float(r[4 * c4 + 1]), c2, -Lv.y));
-          pr[4 * c4 + 2] = ptx::ex2(fmaf(__uint_as_float(r[4 * c4 + 2]), c2, -Lv.z));
-          pr[4 * c4 + 3] = ptx::ex2(fmaf(__uint_as_float(r[4 * c4 + 3]), c2, -Lv.w));
+          // x = S * scale*log2e - lse*log2e on packed fp32x2 (FFMA2)
+          const float2 xa = ptx::ffma2(make_float2(__uint_as_float(r[4 * c4 + 0]), __uint_as_float(r[4 * c4 + 1])),
+                                       make_float2(c2, c2), make_float2(-Lv.x, -Lv.y));
+          const float2 xb = ptx::ffma2(make_float2(__uint_as_float(r[4 * c4 + 2]), __uint_as_float(r[4 * c4 + 3])),
+                                       make_float2(c2, c2), make_float2(-Lv.z, -Lv.w));
+          pr[4 * c4 + 0] = ptx::ex2(xa.x);
+          pr[4 * c4 + 1] = ptx::ex2(xa.y);
+          pr[4 * c4 + 2] = ptx::ex2(xb.x);
+          pr[4 * c4 + 3] = ptx::ex2(xb.y);
         }
       }
       if (!warp_full) {
@@ -413,10 +418,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int j4 = 0; j4 < 16; ++j4) {
         const float4 Dv = dst4[j4];
         const int c = 4 * j4;
-        pk[2 * j4] = ptx::pack_bf16(pr[c] * (__uint_as_float(r[c]) - Dv.x),
-                                    pr[c + 1] * (__uint_as_float(r[c + 1]) - Dv.y));
-        pk[2 * j4 + 1] = ptx::pack_bf16(pr[c + 2] * (__uint_as_float(r[c + 2]) - Dv.z),
-                                        pr[c + 3] * (__uint_as_float(r[c + 3]) - Dv.w));
+        const float2 da = ptx::fmul2(make_float2(pr[c], pr[c + 1]),
+                                     ptx::fadd2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])),
+                                                make_float2(-Dv.x, -Dv.y)));
+        const float2 db = ptx::fmul2(make_float2(pr[c + 2], pr[c + 3]),
+                                     ptx::fadd2(make_float2(__uint_as_float(r[c + 2]), __uint_as_float(r[c + 3])),
+                                                make_float2(-Dv.z, -Dv.w)));
+        pk[2 * j4] = ptx::pack_bf16(da.x, da.y);
+        pk[2 * j4 + 1] = ptx::pack_bf16(db.x, db.y);
       }
       ptx::tmem_st32(tbase + lane_off + kDST + 32 * hq, pk);
       // MN-major A rows of the dQ MMA: row = key, 64 queries (128 B, SW128)

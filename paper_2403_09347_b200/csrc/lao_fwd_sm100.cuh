@@ -51,7 +51,18 @@ struct Params {
   burst_hop hop;
   float scale_log2;
   int first_hop, finalize;
+  long long* trace;   // BURST_TRACE builds only: per-iteration clock64 timeline
 };
+
+#ifdef BURST_TRACE
+#define FTRACE(ev, i)                                                                        \
+  do {                                                                                       \
+    if (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (i) < 64)        \
+      p.trace[(ev) * 64 + (i)] = clock64();                                                  \
+  } while (0)
+#else
+#define FTRACE(ev, i)
+#endif
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   uintptr_t a = reinterpret_cast<uintptr_t>(p);
@@ -192,8 +203,8 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
         const int itv = 2 * j + 1, sv = itv % C::kStages;
         const int itk = 2 * j + 2, sk = itk % C::kStages;
         const bool more = j + 1 < nkv;
-        ptx::mbar_wait(kv_full + sv, (itv / C::kStages) & 1);
-        ptx::mbar_wait(p_full + 0, j & 1);
+        ptx::mbar_wait(kv_full + sv, (itv / C::kStages) & 1); FTRACE(0, j);
+        ptx::mbar_wait(p_full + 0, j & 1); FTRACE(1, j);
         ptx::tc_fence_after();
         pv(0, sv, j > 0);
         if (more) {
@@ -201,7 +212,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
           ptx::tc_fence_after();
           qk(0, sk);
         }
-        ptx::mbar_wait(p_full + 1, j & 1);
+        ptx::mbar_wait(p_full + 1, j & 1); FTRACE(2, j);
         ptx::tc_fence_after();
         pv(1, sv, j > 0);
         commit(kv_empty + sv);
@@ -235,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
     float m_run = -INFINITY, l_run = 0.f;
 
     for (int j = 0; j < nkv; ++j) {
-      ptx::mbar_wait(s_full + g, j & 1);
+      ptx::mbar_wait(s_full + g, j & 1); FTRACE(3 + 8 * g, j);
       ptx::tc_fence_after();
       float s[BN];
       {
@@ -270,7 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
       for (int i = 8; i < BN; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
       const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                              fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-      const float m_tile = mx * c2;
+      const float m_tile = mx * c2; FTRACE(4 + 8 * g, j);
       const bool grow = m_tile > m_run + kRescaleThreshold || (m_run == -INFINITY && m_tile > -INFINITY);
       if (__any_sync(0xffffffffu, grow && j > 0)) {
         const float m_new = grow ? fmaxf(m_tile, m_run) : m_run;
@@ -290,7 +301,10 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
         m_run = fmaxf(m_tile, m_run);
       }
       const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-      float ls8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      // x = S * scale*log2e - m and the row sum on packed fp32x2 (FFMA2 / FADD2)
+      float2 ls4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                       make_float2(0.f, 0.f)};
+      const float2 c2v = make_float2(c2, c2), negm = make_float2(-m_use, -m_use);
       // part of the row's exp2 on the FMA pipe (ex2_poly) when no entry of the warp's
       // tile is masked; masked (-inf) entries must stay exactly 0 -> MUFU only
       const bool poly = !partial;
@@ -299,20 +313,26 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
         uint32_t pk[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          const float x0 = fmaf(s[cc * 64 + 2 * i], c2, -m_use);
-          const float x1 = fmaf(s[cc * 64 + 2 * i + 1], c2, -m_use);
-          const float p0 = poly ? ptx::ex2_mixed(x0, i) : ptx::ex2(x0);
-          const float p1 = poly ? ptx::ex2_mixed(x1, i) : ptx::ex2(x1);
-          ls8[(2 * i) & 7] += p0;
-          ls8[(2 * i + 1) & 7] += p1;
+          const float2 x = ptx::ffma2(make_float2(s[cc * 64 + 2 * i], s[cc * 64 + 2 * i + 1]), c2v, negm);
+          float p0, p1;
+          if (poly && BURST_POLY_CNT > 0 && (i % BURST_POLY_MOD) < BURST_POLY_CNT) {
+            const float2 pp = ptx::ex2_poly2(x);
+            p0 = pp.x;
+            p1 = pp.y;
+          } else {
+            p0 = ptx::ex2(x.x);
+            p1 = ptx::ex2(x.y);
+          }
+          ls4[i & 3] = ptx::fadd2(ls4[i & 3], make_float2(p0, p1));
           pk[i] = ptx::pack_bf16(p0, p1);
         }
         ptx::tmem_st32(tS + cc * 32, pk);
       }
-      l_run += ((ls8[0] + ls8[1]) + (ls8[2] + ls8[3])) + ((ls8[4] + ls8[5]) + (ls8[6] + ls8[7]));
+      const float2 lsa = ptx::fadd2(ptx::fadd2(ls4[0], ls4[1]), ptx::fadd2(ls4[2], ls4[3]));
+      l_run += lsa.x + lsa.y;
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(p_full + g);
+      ptx::mbar_arrive(p_full + g); FTRACE(5 + 8 * g, j);
     }
 
     // ------------------------------------------------------------ epilogue

@@ -388,6 +388,41 @@ __device__ __forceinline__ float ex2_poly(float x) {
 __device__ __forceinline__ float ex2_mixed(float x, int idx) {
   return (BURST_POLY_CNT > 0 && (idx % BURST_POLY_MOD) < BURST_POLY_CNT) ? ex2_poly(x) : ex2(x);
 }
+// Packed fp32x2 arithmetic (sm_100: FFMA2 / FADD2 issue two lanes' worth per
+// instruction, halving the issue slots of the softmax's elementwise work).
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&d);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return *reinterpret_cast<float2*>(&d);
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return *reinterpret_cast<float2*>(&d);
+}
+// ex2_poly on a pair (FADD2 / FFMA2 for the split and the polynomial).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x = make_float2(fmaxf(x.x, -125.f), fmaxf(x.y, -125.f));
+  const float2 magic = make_float2(12582912.f, 12582912.f), nmagic = make_float2(-12582912.f, -12582912.f);
+  const float2 j = fadd2(x, magic);
+  const float2 n = fadd2(j, nmagic);
+  const float2 f = fadd2(x, make_float2(-n.x, -n.y));
+  float2 p = ffma2(make_float2(0.05508868380751114f, 0.05508868380751114f), f,
+                   make_float2(0.24260405145947936f, 0.24260405145947936f));
+  p = ffma2(p, f, make_float2(0.6932762416819607f, 0.6932762416819607f));
+  p = ffma2(p, f, make_float2(0.9999289403695112f, 0.9999289403695112f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(j.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(j.y) << 23)));
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
