@@ -45,6 +45,12 @@ CONFIGS = {
     "c4": dict(workload="causal LLaMA-7B-shaped attention, seq 128K, zigzag partition, bf16, "
                         "fwd+bwd (BASELINE configs[3])", seq=131072, heads=32, d=128, batch=1,
                causal=True),
+    "c3_sparse": dict(workload="C3 shape with a block-sparse grid mask: 32x32 cells of 4096 "
+                               "positions, checkerboard of skipped cells (50% of the score matrix), "
+                               "non-causal (reference BlockGrid, masking.py:33-147)",
+                      seq=131072, heads=32, d=128, batch=1, causal=False,
+                      mask={"n_query_blocks": 32, "n_key_blocks": 32,
+                            "skip": [[a, b] for a in range(32) for b in range(32) if (a + b) % 2]}),
     "c5_512k": dict(workload="LLaMA-13B-shaped attention, 40 heads x d128, seq 512K, bf16, "
                              "fwd+bwd (BASELINE configs[4])", seq=524288, heads=40, d=128,
                     batch=1, causal=False),
@@ -170,8 +176,16 @@ def run_reference(args, cfg, rank):
     print(json.dumps(line), flush=True)
 
 
+def _density(cfg):
+    """Fraction of the score matrix a grid mask leaves visible (1 without a mask)."""
+    m = cfg.get("mask")
+    if not m:
+        return 1.0
+    return 1.0 - len(m["skip"]) / (m["n_query_blocks"] * m["n_key_blocks"])
+
+
 def _flops(cfg):
-    f = 14.0 * cfg["batch"] * cfg["heads"] * cfg["seq"] ** 2 * cfg["d"]
+    f = 14.0 * cfg["batch"] * cfg["heads"] * cfg["seq"] ** 2 * cfg["d"] * _density(cfg)
     return f / 2 if cfg["causal"] else f
 
 
@@ -242,7 +256,7 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     def step(qq, kk, vv, dd, recorders=None):
         o, lse = burst_attn_func(qq, kk, vv, causal=causal, zigzag=zigzag, _kernels=kern,
-                                 comm=args.comm, _recorders=recorders)
+                                 comm=args.comm, mask=cfg.get("mask"), _recorders=recorders)
         grads = torch.autograd.grad(o, (qq, kk, vv), dd)
         return o, grads
 
@@ -419,6 +433,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded N(0,1) q/k/v/dO)",
         "config": {"workload": cfg["workload"], "seq": N, "heads": H, "head_dim": D, "batch": B,
+                   "visible_fraction": _density(cfg) * (0.5 if causal else 1.0),
                    "causal": causal, "partition": "zigzag" if zigzag else "contiguous",
                    "parallelism": f"ring sp{world}", "comm": args.comm if world > 1 else None,
                    "l2": "inputs larger than L2 "

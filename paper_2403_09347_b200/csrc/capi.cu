@@ -174,10 +174,16 @@ int launch_fwd_bf16(const burst_hop* h, const void* q, const void* k, const void
 #endif
   static std::once_flag once;
   static int attr_rc = 0;
-  std::call_once(once, [] { attr_rc = set_smem(fwd::lao_fwd_kernel<D>, fwd::Cfg<D>::kSmemBytes); });
+  std::call_once(once, [] {
+    attr_rc = set_smem(fwd::lao_fwd_kernel<D, false>, fwd::Cfg<D>::kSmemBytes);
+    if (!attr_rc) attr_rc = set_smem(fwd::lao_fwd_kernel<D, true>, fwd::Cfg<D>::kSmemBytes);
+  });
   if (attr_rc) return attr_rc;
   dim3 grid((unsigned)ceil_div(h->q_len, 2 * fwd::BM), h->heads, h->batch);
-  fwd::lao_fwd_kernel<D><<<grid, fwd::kThreads, fwd::Cfg<D>::kSmemBytes, st>>>(p);
+  if (h->grid_skip)
+    fwd::lao_fwd_kernel<D, true><<<grid, fwd::kThreads, fwd::Cfg<D>::kSmemBytes, st>>>(p);
+  else
+    fwd::lao_fwd_kernel<D, false><<<grid, fwd::kThreads, fwd::Cfg<D>::kSmemBytes, st>>>(p);
   CHECK_LAUNCH();
   return BURST_OK;
 }
@@ -320,10 +326,16 @@ int launch_bwd4_bf16(const burst_hop* h, const void* q, const void* k, const voi
 #endif
   static std::once_flag once;
   static int attr_rc = 0;
-  std::call_once(once, [] { attr_rc = set_smem(bwd4::lao_bwd4_kernel<D>, bwd4::Cfg<D>::kSmemBytes); });
+  std::call_once(once, [] {
+    attr_rc = set_smem(bwd4::lao_bwd4_kernel<D, false>, bwd4::Cfg<D>::kSmemBytes);
+    if (!attr_rc) attr_rc = set_smem(bwd4::lao_bwd4_kernel<D, true>, bwd4::Cfg<D>::kSmemBytes);
+  });
   if (attr_rc) return attr_rc;
   dim3 grid((unsigned)ceil_div(h->k_len, bwd4::BN), h->heads, h->batch);
-  bwd4::lao_bwd4_kernel<D><<<grid, bwd4::kThreads, bwd4::Cfg<D>::kSmemBytes, st>>>(p);
+  if (h->grid_skip)
+    bwd4::lao_bwd4_kernel<D, true><<<grid, bwd4::kThreads, bwd4::Cfg<D>::kSmemBytes, st>>>(p);
+  else
+    bwd4::lao_bwd4_kernel<D, false><<<grid, bwd4::kThreads, bwd4::Cfg<D>::kSmemBytes, st>>>(p);
   CHECK_LAUNCH();
   return BURST_OK;
 }

@@ -86,7 +86,9 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 #define BTRACE4(ev, i)
 #endif
 
-template <int D>
+// kGrid: the hop carries a block-sparse grid mask (tile skipping + element masks);
+// the instantiation without it keeps the dense loops free of the skip bookkeeping.
+template <int D, bool kGrid>
 __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_constant__ Params p) {
   using C = Cfg<D>;
   extern __shared__ uint8_t smem_raw[];
@@ -143,6 +145,20 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
   // profiles/r01_rotation_exp.txt).
   const int rot = nq > 0 ? (int)((blockIdx.x * 7u) % (unsigned)nq) : 0;
   auto qtile = [&](int i) -> int64_t { int j = i + rot; if (j >= nq) j -= nq; return qs + (int64_t)j * BM; };
+  // Block-sparse grid: query tiles whose every (query, key) pair with this CTA's keys
+  // lies in skipped cells are skipped by every role.  Roles count LIVE tiles (stages,
+  // barrier parities); the producer, P/dS and drain map them back to tile indices.
+  const int64_t krows = (k0 + BN < k_end ? k0 + BN : k_end) - k0;
+  auto live = [&](int i) -> bool {
+    if (!kGrid) return true;
+    const int64_t q0 = qtile(i);
+    return grid_rect_live(hp, q0, (q0 + BM < q_end ? q0 + BM : q_end) - q0, k0, krows);
+  };
+  auto next_live = [&](int i) -> int {
+    while (i < nq && !live(i)) ++i;
+    return i;
+  };
+  int nlive = nq;   // kGrid: counted cooperatively by the whole CTA below
 
   if (warp == 12) {
     if (lane == 0) {
@@ -170,35 +186,44 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
     __syncwarp();
     ptx::tmem_alloc(tmem_holder, 512);
   }
+  if (kGrid) {
+    if (threadIdx.x == 0) tmem_holder[1] = 0;
+    __syncthreads();
+    int mine = 0;
+    for (int i = threadIdx.x; i < nq; i += kThreads) mine += live(i) ? 1 : 0;
+    mine = __reduce_add_sync(0xffffffffu, mine);
+    if (lane == 0 && mine) atomicAdd(tmem_holder + 1, (uint32_t)mine);
+  }
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tbase = *tmem_holder;
+  if (kGrid) nlive = (int)tmem_holder[1];
   constexpr uint32_t kS = 0, kDP = 128, kDV = 256, kDK = 256 + D;
   if (warp >= 12) {
    ptx::regs_dec<80>();
 #ifdef BURST_TRACE
    if (warp == 14 && lane == 0 && blockIdx.x == 0) {
      // observer: completion times of the MMA groups (tensor-pipe timeline)
-     for (int i = 0; i < nq && i < 64; ++i) {
+     for (int i = 0; i < nlive && i < 64; ++i) {
        ptx::mbar_wait(s_full, i & 1); BTRACE4(16, i);
        ptx::mbar_wait(do_empty, i & 1); BTRACE4(17, i);     // dV_i done
        ptx::mbar_wait(dq_full, i & 1); BTRACE4(18, i);      // dK_i, dQ_i done
-       if (i + 1 < nq) { ptx::mbar_wait(dp_full, (i + 1) & 1); BTRACE4(19, i); }   // dP^T_{i+1} done
+       if (i + 1 < nlive) { ptx::mbar_wait(dp_full, (i + 1) & 1); BTRACE4(19, i); }   // dP^T_{i+1} done
      }
    }
 #endif
    if (warp == 12) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0 && nq > 0) {
+    if (lane == 0 && nlive > 0) {
       ptx::mbar_expect_tx(kv_full, 2 * C::kTileBytes);
       for (int x = 0; x < C::kBoxes; ++x) {
         ptx::tma_load_4d(sK + x * C::kBoxBytes, &p.tm_k, kv_full, x * 64, h, (int)k0, b);
         ptx::tma_load_4d(sV + x * C::kBoxBytes, &p.tm_v, kv_full, x * 64, h, (int)k0, b);
       }
-      auto load_q = [&](int j) {
+      auto load_q = [&](int j, int ti) {   // j = live index, ti = query tile index
         const int s = j & 1;
-        const int64_t q0 = qtile(j);
+        const int64_t q0 = qtile(ti);
         ptx::mbar_wait(qdo_empty + s, ((j >> 1) & 1) ^ 1);
         ptx::mbar_expect_tx(qdo_full + s, C::kTileBytes + C::kStatBytes);
         for (int x = 0; x < C::kBoxes; ++x)
@@ -209,18 +234,19 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
         bulk_load(sStat + s * 2 * BM + BM, st + (int64_t)hp.batch * hp.heads * NTq * 128, BM * 4,
                   qdo_full + s);
       };
-      auto load_do = [&](int j) {
+      auto load_do = [&](int j, int ti) {
         ptx::mbar_wait(do_empty, (j & 1) ^ 1);
         ptx::mbar_expect_tx(do_full, C::kTileBytes);
         for (int x = 0; x < C::kBoxes; ++x)
-          ptx::tma_load_4d(sdO + x * C::kBoxBytes, &p.tm_do, do_full, x * 64, h, (int)qtile(j), b);
+          ptx::tma_load_4d(sdO + x * C::kBoxBytes, &p.tm_do, do_full, x * 64, h, (int)qtile(ti), b);
       };
-      load_q(0);
-      load_do(0);
-      if (nq > 1) load_q(1);
-      for (int i = 0; i < nq; ++i) {      // release order: dO after dV_i, Q stage after dK_i
-        if (i + 1 < nq) load_do(i + 1);
-        if (i + 2 < nq) load_q(i + 2);
+      int tq = next_live(0), td = tq;      // next tile of the Q and of the dO load stream
+      load_q(0, tq); tq = next_live(tq + 1);
+      load_do(0, td); td = next_live(td + 1);
+      if (nlive > 1) { load_q(1, tq); tq = next_live(tq + 1); }
+      for (int i = 0; i < nlive; ++i) {      // release order: dO after dV_i, Q stage after dK_i
+        if (i + 1 < nlive) { load_do(i + 1, td); td = next_live(td + 1); }
+        if (i + 2 < nlive) { load_q(i + 2, tq); tq = next_live(tq + 1); }
       }
     }
    } else if (warp == 13) {
@@ -230,7 +256,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
     // dQ_i has been drained to registers.  The whole warp runs the loop (uniform
     // control flow keeps descriptors in uniform registers); one elected lane issues
     // each MMA group and its commits.  Descriptors: base + (byte offset >> 4).
-    if (nq > 0) {
+    if (nlive > 0) {
       constexpr uint32_t id_kk = ptx::make_idesc_bf16(BN, BM, 0, 0);   // S^T, dP^T
       constexpr uint32_t id_kmn = ptx::make_idesc_bf16(BN, D, 0, 1);   // dV, dK (B MN-major)
       constexpr uint32_t id_mnmn = ptx::make_idesc_bf16(BM, D, 1, 1);  // dQ (A, B MN-major)
@@ -287,9 +313,9 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
       ptx::mbar_wait(do_full, 0);
       ptx::tc_fence_after();
       dpt_mma();
-      for (int i = 0; i < nq; ++i) {
+      for (int i = 0; i < nlive; ++i) {
         const int s = i & 1;
-        const bool more = i + 1 < nq;
+        const bool more = i + 1 < nlive;
         // dV += P^T dO   (A = P^T from TMEM: query half h at S^T columns [64h, 64h+32))
         ptx::mbar_wait(p_full, i & 1); BTRACE4(0, i);
         ptx::tc_fence_after();
@@ -335,18 +361,18 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const int64_t krow = k0 + t;
     const bool kvalid = krow < k_end && krow < hp.n_k;
-    const int64_t kpos = (hp.causal || hp.grid_skip) ? pos_of(hp.k_map, kvalid ? krow : k0) : 0;
+    const int64_t kpos = (hp.causal || kGrid) ? pos_of(hp.k_map, kvalid ? krow : k0) : 0;
     const int64_t qfirst = hp.causal ? count_le(hp.q_map, hp.n_q, kpos - 1) : 0;
     const float c2 = p.scale_log2;
-    for (int i = 0; i < nq; ++i) {
+    for (int i = 0, ti = next_live(0); i < nlive; ++i, ti = next_live(ti + 1)) {
       const int s = i & 1;
-      const int64_t q0 = qtile(i) + 64 * hq;
+      const int64_t q0 = qtile(ti) + 64 * hq;
       // visible query columns of this key row within the half: [lo, hi)
       int64_t lo64 = qfirst - q0, hi64 = q_end - q0;
       const int lo = lo64 < 0 ? 0 : (lo64 > 64 ? 64 : (int)lo64);
       const int hi = !kvalid ? 0 : (hi64 > 64 ? 64 : (hi64 < 0 ? 0 : (int)hi64));
       uint64_t gq = 0;   // block-sparse grid: hidden query columns of this half
-      if (hp.grid_skip) {
+      if (kGrid) {
         const int nv = hi64 > 64 ? 64 : (hi64 < 0 ? 0 : (int)hi64);
         if (nv > 0) gq = grid_query_bits(hp, q0, nv, kpos);
       }
@@ -438,7 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
       ptx::mbar_arrive(ds_full); if (hq == 0) BTRACE4(6, i); else BTRACE4(23, i);
     }
     // -------------------------------------------------------- dK / dV epilogue
-    if (nq > 0) {
+    if (nlive > 0) {
       ptx::mbar_wait(dkv_full, 0);
       ptx::tc_fence_after();
     }
@@ -449,7 +475,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
 #pragma unroll 1
       for (int cc = 0; cc < D / 32; ++cc) {
         uint32_t r[32];
-        if (nq > 0) {
+        if (nlive > 0) {
           ptx::tmem_ld32(tbase + lane_off + col0 + cc * 32, r);
           ptx::tmem_wait_ld();
           ptx::reg_fence(r);
@@ -480,8 +506,8 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
     const int t = threadIdx.x & 127;           // query row within the tile
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     float4* stg = reinterpret_cast<float4*>(sStage);
-    for (int i = 0; i < nq; ++i) {
-      const int64_t q0 = qtile(i);
+    for (int i = 0, ti = next_live(0); i < nlive; ++i, ti = next_live(ti + 1)) {
+      const int64_t q0 = qtile(ti);
       const bool qvalid = q0 + t < q_end && q0 + t < hp.n_q;
       ptx::mbar_wait(dq_full, i & 1); BTRACE4(7, i);
       ptx::tc_fence_after();

@@ -71,7 +71,9 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>(a + pad);
 }
 
-template <int D>
+// kGrid: the hop carries a block-sparse grid mask (tile skipping + element masks);
+// the instantiation without it keeps the dense loops free of the skip bookkeeping.
+template <int D, bool kGrid>
 __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_constant__ Params p) {
   using C = Cfg<D>;
   extern __shared__ uint8_t smem_raw[];
@@ -106,6 +108,20 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
     if (kspan < 0) kspan = 0;
   }
   const int nkv = (int)ceil_div(kspan, BN);
+  // Block-sparse grid: KV tiles whose every (query, key) pair lies in skipped cells
+  // are skipped by every role (each evaluates the same predicate).
+  const int64_t qrows = (row0 + 2 * BM < q_end ? row0 + 2 * BM : q_end) - row0;
+  auto live = [&](int j) -> bool {
+    if (!kGrid) return true;
+    const int64_t kr = kspan - (int64_t)j * BN;
+    return grid_rect_live(hp, row0, qrows, hp.k_begin + (int64_t)j * BN, kr < BN ? kr : BN);
+  };
+  auto next_live = [&](int j) -> int {
+    while (j < nkv && !live(j)) ++j;
+    return j;
+  };
+  const int first = next_live(0);
+  const bool any = first < nkv;
 
   if (warp == 8) {
     if (lane == 0) {
@@ -135,14 +151,14 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
    ptx::regs_dec<88>();
    if (warp == 8) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0 && nkv > 0) {
+    if (lane == 0 && any) {
       ptx::mbar_expect_tx(q_full, 2 * C::kTileBytes);
       for (int t = 0; t < 2; ++t)
         for (int x = 0; x < C::kBoxes; ++x)
           ptx::tma_load_4d(sQ + t * C::kTileBytes + x * C::kBoxBytes, &p.tm_q, q_full, x * 64, h,
                            (int)(row0 + t * BM), b);
       int it = 0;
-      for (int j = 0; j < nkv; ++j) {
+      for (int j = first; j < nkv; j = next_live(j + 1)) {
         const int krow = (int)(hp.k_begin + (int64_t)j * BN);
         for (int kv = 0; kv < 2; ++kv, ++it) {
           const int s = it % C::kStages;
@@ -160,7 +176,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
     // ------------------------------------------------------------ MMA issuer
     // Whole warp runs the loop (uniform control flow keeps descriptors in uniform
     // registers); one elected lane issues each MMA group and its commits.
-    if (nkv > 0) {
+    if (any) {
       constexpr uint32_t idesc_qk = ptx::make_idesc_bf16(BM, BN, 0, 0);
       constexpr uint32_t idesc_pv = ptx::make_idesc_bf16(BM, D, 0, 1);
       const uint64_t dQk = ptx::make_sdesc(ptx::smem_u32(sQ), 0, 1024);
@@ -199,27 +215,30 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
       qk(0, 0);
       qk(1, 0);
       commit(kv_empty + 0);
-      for (int j = 0; j < nkv; ++j) {
-        const int itv = 2 * j + 1, sv = itv % C::kStages;
-        const int itk = 2 * j + 2, sk = itk % C::kStages;
-        const bool more = j + 1 < nkv;
-        ptx::mbar_wait(kv_full + sv, (itv / C::kStages) & 1); FTRACE(0, j);
-        ptx::mbar_wait(p_full + 0, j & 1); FTRACE(1, j);
+      // jj = index among the live KV tiles (stage / parity counter); j = tile index
+      for (int j = first, jj = 0; j < nkv; ++jj) {
+        const int jn = next_live(j + 1);
+        const int itv = 2 * jj + 1, sv = itv % C::kStages;
+        const int itk = 2 * jj + 2, sk = itk % C::kStages;
+        const bool more = jn < nkv;
+        ptx::mbar_wait(kv_full + sv, (itv / C::kStages) & 1); FTRACE(0, jj);
+        ptx::mbar_wait(p_full + 0, jj & 1); FTRACE(1, jj);
         ptx::tc_fence_after();
-        pv(0, sv, j > 0);
+        pv(0, sv, jj > 0);
         if (more) {
           ptx::mbar_wait(kv_full + sk, (itk / C::kStages) & 1);
           ptx::tc_fence_after();
           qk(0, sk);
         }
-        ptx::mbar_wait(p_full + 1, j & 1); FTRACE(2, j);
+        ptx::mbar_wait(p_full + 1, jj & 1); FTRACE(2, jj);
         ptx::tc_fence_after();
-        pv(1, sv, j > 0);
+        pv(1, sv, jj > 0);
         commit(kv_empty + sv);
         if (more) {
           qk(1, sk);
           commit(kv_empty + sk);
         }
+        j = jn;
       }
       commit(o_full);
     }
@@ -245,8 +264,8 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
     const float c2 = p.scale_log2;
     float m_run = -INFINITY, l_run = 0.f;
 
-    for (int j = 0; j < nkv; ++j) {
-      ptx::mbar_wait(s_full + g, j & 1); FTRACE(3 + 8 * g, j);
+    for (int j = first, jj = 0; j < nkv; j = next_live(j + 1), ++jj) {
+      ptx::mbar_wait(s_full + g, jj & 1); FTRACE(3 + 8 * g, jj);
       ptx::tc_fence_after();
       float s[BN];
       {
@@ -261,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
       }
       const int64_t nvalid = lim - (int64_t)j * BN;
       uint64_t gk0 = 0, gk1 = 0;   // block-sparse grid: hidden key columns of this row
-      if (hp.grid_skip) {
+      if (kGrid) {
         const int nv = nvalid > BN ? BN : (nvalid < 0 ? 0 : (int)nvalid);
         const int64_t kt0 = hp.k_begin + (int64_t)j * BN;
         if (nv > 0) gk0 = grid_key_bits(hp, qpos, kt0, nv < 64 ? nv : 64);
@@ -281,9 +300,9 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
       for (int i = 8; i < BN; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
       const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                              fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-      const float m_tile = mx * c2; FTRACE(4 + 8 * g, j);
+      const float m_tile = mx * c2; FTRACE(4 + 8 * g, jj);
       const bool grow = m_tile > m_run + kRescaleThreshold || (m_run == -INFINITY && m_tile > -INFINITY);
-      if (__any_sync(0xffffffffu, grow && j > 0)) {
+      if (__any_sync(0xffffffffu, grow && jj > 0)) {
         const float m_new = grow ? fmaxf(m_tile, m_run) : m_run;
         const float alpha = (m_run == -INFINITY) ? 0.f : ptx::ex2(m_run - m_new);
 #pragma unroll
@@ -332,11 +351,11 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
       l_run += lsa.x + lsa.y;
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(p_full + g); FTRACE(5 + 8 * g, j);
+      ptx::mbar_arrive(p_full + g); FTRACE(5 + 8 * g, jj);
     }
 
     // ------------------------------------------------------------ epilogue
-    if (nkv > 0) {
+    if (any) {
       ptx::mbar_wait(o_full, 0);
       ptx::tc_fence_after();
     }
@@ -356,7 +375,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
 #pragma unroll
     for (int cc = 0; cc < D / 32; ++cc) {
       uint32_t r[32];
-      if (nkv > 0) {
+      if (any) {
         ptx::tmem_ld32(tO + cc * 32, r);
         ptx::tmem_wait_ld();
       } else {

@@ -64,6 +64,8 @@ class GridMask:
     def bind(self, total: int) -> "GridMask":
         """The grid over a global sequence of `total` positions (validate's
         divisibility rule, masking.py:135-139)."""
+        if total >= 2 ** 31:
+            raise MaskError("grid masks support global lengths below 2^31 positions")
         if total % self.n_query_blocks or total % self.n_key_blocks:
             raise MaskError(f"grid {self.n_query_blocks}x{self.n_key_blocks} does not divide "
                             f"score matrix {total}x{total}")
@@ -91,6 +93,10 @@ class GridMask:
     def validate(self, causal: bool, real_rows: int | None = None) -> None:
         """Reject masks that leave a real query row with no visible key
         (BlockMask.validate, masking.py:132-147)."""
+        key = (causal, real_rows)
+        done = _VALIDATED.setdefault(self, set())
+        if key in done:
+            return
         n = self.total
         rows = n if real_rows is None else real_rows
         t = self.table()
@@ -107,6 +113,7 @@ class GridMask:
                     raise MaskError(f"query row {r0} has every key masked out")
             elif not open_cols.any():
                 raise MaskError(f"query row {r0} has every key masked out")
+        done.add(key)
 
     def device_table(self, device):
         """Cached uint8 [nqb * nkb] table on `device` (the burst_hop grid_skip)."""
@@ -119,3 +126,4 @@ class GridMask:
 
 
 _TABLES: dict = {}
+_VALIDATED: dict = {}

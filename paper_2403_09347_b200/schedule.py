@@ -152,9 +152,11 @@ def hop_flops(plan: HopPlan, batch: int, heads: int, d: int) -> tuple[float, flo
     counting only visible score entries for DIAG hops."""
     if plan.skip:
         return 0.0, 0.0
-    if plan.causal:
-        qp = plan.q_map.positions(plan.q_len)
-        kp = plan.k_map.positions(plan.k_len)
+    if plan.grid is not None:
+        area = _grid_area(plan)
+    elif plan.causal:
+        qp = plan.q_map.positions(plan.q_begin + plan.q_len)[plan.q_begin:]
+        kp = plan.k_map.positions(plan.k_begin + plan.k_len)[plan.k_begin:]
         import bisect
         ks = sorted(kp)
         area = sum(bisect.bisect_right(ks, p) for p in qp)
@@ -162,6 +164,27 @@ def hop_flops(plan: HopPlan, batch: int, heads: int, d: int) -> tuple[float, flo
         area = plan.q_len * plan.k_len
     f = 4.0 * batch * heads * area * d
     return f, 2.5 * f
+
+
+def _grid_area(plan: HopPlan) -> int:
+    """Visible (query, key) pairs of a hop under its grid mask (and causal rule),
+    counted per grid cell (no N x N map)."""
+    import numpy as np
+    g = plan.grid
+    qp = np.asarray(plan.q_map.positions(plan.q_begin + plan.q_len)[plan.q_begin:], dtype=np.int64)
+    kp = np.asarray(plan.k_map.positions(plan.k_begin + plan.k_len)[plan.k_begin:], dtype=np.int64)
+    qc = np.minimum(qp // g.qcell, g.n_query_blocks - 1)
+    kc = np.minimum(kp // g.kcell, g.n_key_blocks - 1)
+    open_ = (g.table() == 0).astype(np.int64)
+    if not plan.causal:
+        qn = np.bincount(qc, minlength=g.n_query_blocks)
+        kn = np.bincount(kc, minlength=g.n_key_blocks)
+        return int(qn @ open_ @ kn)
+    area = 0
+    for c in np.unique(kc):
+        ks = np.sort(kp[kc == c])
+        area += int((np.searchsorted(ks, qp, side="right") * open_[qc, c]).sum())
+    return area
 
 
 # ---------------------------------------------------------------------------
