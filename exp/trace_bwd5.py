@@ -2,7 +2,7 @@
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ["BURST_LIB"] = os.path.join(os.path.dirname(os.path.abspath(__file__)), os.environ.get("TRACE_LIB", "lib_trace.so"))
-os.environ["BURST_BWD_KERNEL"] = "5"
+os.environ["BURST_BWD_KERNEL"] = os.environ.get("TRACE_KERNEL", "5")
 import numpy as np, torch
 from paper_2403_09347_b200 import _lib
 from paper_2403_09347_b200.kernels import CudaKernels

@@ -16,6 +16,7 @@
 #include "lao_bwd3_sm100.cuh"
 #include "lao_bwd4_sm100.cuh"
 #include "lao_bwd5_sm100.cuh"
+#include "lao_bwd6_sm100.cuh"
 #include "lao_bwd_sm100.cuh"
 #include "lao_fwd_sm100.cuh"
 #include "simt_f32.cuh"
@@ -263,6 +264,37 @@ int launch_bwd5_bf16(const burst_hop* h, const void* q, const void* k, const voi
   return BURST_OK;
 }
 
+// CTA-pair backward with the dS exchange and dQ off the critical path (variant 6).
+int launch_bwd6_bf16(const burst_hop* h, const void* q, const void* k, const void* v, const void* dout,
+                     const float* stats, float* dq_acc, float* dk, float* dv, int acc, cudaStream_t st) {
+  bwd6::Params p;
+  memset(&p, 0, sizeof(p));
+  int rc;
+  if ((rc = make_tmap(&p.tm_q128, q, h->n_q, h->heads, 128, h->batch))) return rc;
+  if ((rc = make_tmap(&p.tm_q64, q, h->n_q, h->heads, 128, h->batch, 64))) return rc;
+  if ((rc = make_tmap(&p.tm_do128, dout, h->n_q, h->heads, 128, h->batch))) return rc;
+  if ((rc = make_tmap(&p.tm_do64, dout, h->n_q, h->heads, 128, h->batch, 64))) return rc;
+  if ((rc = make_tmap(&p.tm_k, k, h->n_k, h->heads, 128, h->batch))) return rc;
+  if ((rc = make_tmap(&p.tm_v, v, h->n_k, h->heads, 128, h->batch))) return rc;
+  if ((rc = make_tmap_tl(&p.tm_dq, dq_acc, h->n_q, h->heads, 128, h->batch))) return rc;
+  p.stats = stats; p.dq_acc = dq_acc; p.dk_acc = dk; p.dv_acc = dv;
+  p.hop = *h;
+  p.scale_log2 = h->softmax_scale * kLog2e;
+  p.scale = h->softmax_scale;
+  p.accumulate = acc;
+#ifdef BURST_TRACE
+  p.trace = trace_buffer();
+#endif
+  static std::once_flag once;
+  static int attr_rc = 0;
+  std::call_once(once, [] { attr_rc = set_smem(bwd6::lao_bwd6_kernel, bwd6::kSmemBytes); });
+  if (attr_rc) return attr_rc;
+  dim3 grid((unsigned)(2 * ceil_div(h->k_len, 2 * bwd6::BN)), h->heads, h->batch);
+  bwd6::lao_bwd6_kernel<<<grid, bwd6::kThreads, bwd6::kSmemBytes, st>>>(p);
+  CHECK_LAUNCH();
+  return BURST_OK;
+}
+
 // Backward kernel variant for bf16 (BURST_BWD_KERNEL: 1 = single CTA + red.global,
 // 2 = alias of 5, 3 = single CTA + SMEM-staged TMA bulk reductions, 4 = variant 3 with two
 // P/dS warpgroups and a double-buffered dQ drain, 5 = CTA pair with two P/dS warpgroups,
@@ -272,7 +304,7 @@ std::atomic<int> g_bwd_override{0};   // burst_set_bwd_variant (0 = env / defaul
 int bwd_variant() {
   static int v = [] {
     const char* e = getenv("BURST_BWD_KERNEL");
-    return (e && e[0] >= '1' && e[0] <= '5') ? e[0] - '0' : 4;
+    return (e && e[0] >= '1' && e[0] <= '6') ? e[0] - '0' : 4;
   }();
   const int o = g_bwd_override.load(std::memory_order_relaxed);
   return o ? o : v;
@@ -481,6 +513,7 @@ int burst_lao_bwd(const burst_hop* hop, const void* q, const void* k, const void
       if (var == 4) return launch_bwd4_bf16<128>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
       if (var == 2 || var == 5)   // 2: the first pair kernel, superseded by bwd5
         return launch_bwd5_bf16(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
+      if (var == 6) return launch_bwd6_bf16(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
       return launch_bwd_bf16<128>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
     }
     if (var == 3) return launch_bwd3_bf16<64>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
@@ -542,7 +575,7 @@ int burst_tl_sum(int dtype, int batch, int heads, int head_dim, int64_t n, const
 }
 
 int burst_set_bwd_variant(int variant) {
-  if (variant < 0 || variant > 5) return fail(BURST_E_SHAPE, "backward variant must be 0 (default) .. 5");
+  if (variant < 0 || variant > 6) return fail(BURST_E_SHAPE, "backward variant must be 0 (default) .. 6");
   g_bwd_override.store(variant, std::memory_order_relaxed);
   return BURST_OK;
 }

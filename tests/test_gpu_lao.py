@@ -246,7 +246,7 @@ def bwd_variant():
     _lib.call("burst_set_bwd_variant", 0)
 
 
-@pytest.mark.parametrize("variant", [1, 3, 5])
+@pytest.mark.parametrize("variant", [1, 3, 5, 6])
 @pytest.mark.parametrize("world,causal,zigzag", [(1, False, False), (2, True, True),
                                                  (4, False, False)])
 def test_backward_variants_parity(bwd_variant, variant, world, causal, zigzag):
