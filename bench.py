@@ -283,8 +283,10 @@ def run_ours(args, cfg, rank, world, local_rank):
     kern.on = False
     ms = start.elapsed_time(end) / args.steps
     launches = kern.launches
+    # collectives on small host-side values: CUDA tensors for NCCL, CPU for gloo
+    cdev = dev if world > 1 and dist.get_backend() == "nccl" else "cpu"
     if world > 1:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms], device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = t.item()
 
@@ -309,7 +311,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         torch.cuda.synchronize()
         sf, sb = comm_summary(recs[0].events()), comm_summary(recs[1].events())
         vals = torch.tensor([sf["send_us"], sf["hidden_us"], sb["send_us"], sb["hidden_us"]],
-                            device=dev, dtype=torch.float64)
+                            device=cdev, dtype=torch.float64)
         allv = [torch.zeros_like(vals) for _ in range(world)]
         dist.all_gather(allv, vals)
         tot = torch.stack(allv).sum(0).tolist()
@@ -380,7 +382,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     barrier()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
     if world > 1:
-        t = torch.tensor([e2e_ms], device=dev)
+        t = torch.tensor([e2e_ms], device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = t.item()
     tensor_bytes = B * n * H * D * 2
@@ -471,11 +473,20 @@ def main():
         run_reference(args, cfg, rank)
         return
     import torch
+    # Test hook: BURST_BENCH_ONE_GPU=1 puts every rank on device 0 (exercises the N > 1
+    # code paths on a one-GPU box; use with BURST_BENCH_BACKEND=gloo and --comm ce,
+    # since NCCL refuses two ranks on one device).  Not a measurement configuration.
+    if os.environ.get("BURST_BENCH_ONE_GPU") == "1":
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("BURST_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     if args.gpus != world and world > 1:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
     run_ours(args, cfg, rank, world, local_rank)
