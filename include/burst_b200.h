@@ -132,6 +132,10 @@ BURST_API int burst_tl_sum(int dtype, int batch, int heads, int head_dim, int64_
  * 5 (or 2) = bwd5 (CTA pair, dS^T in TMEM).  Process-wide. */
 BURST_API int burst_set_bwd_variant(int variant);
 
+/* Select the bf16 head_dim-128 forward kernel: 0 = default (BURST_FWD_KERNEL env or 1),
+ * 1 = 128-key tiles, 2 = 64-key tiles with double-buffered scores (dense hops only). */
+BURST_API int burst_set_fwd_variant(int variant);
+
 /* Non-zero device-side flags raised by kernels since the last call (bit 0: a
  * row with no visible key, bit 1: non-finite output).  Synchronises `stream`. */
 BURST_API int burst_read_flags(void* stream, int* flags_out);

@@ -63,6 +63,7 @@ _SIGS = {
                       _c_p], _c_i32),
     "burst_read_flags": ([_c_p, ctypes.POINTER(_c_i32)], _c_i32),
     "burst_set_bwd_variant": ([_c_i32], _c_i32),
+    "burst_set_fwd_variant": ([_c_i32], _c_i32),
     "burst_ipc_handle_bytes": ([], _c_sz),
     "burst_ipc_alloc": ([_c_sz, ctypes.POINTER(_c_p)], _c_i32),
     "burst_ipc_free": ([_c_p], _c_i32),

@@ -19,6 +19,7 @@
 #include "lao_bwd6_sm100.cuh"
 #include "lao_bwd_sm100.cuh"
 #include "lao_fwd_sm100.cuh"
+#include "lao_fwd2_sm100.cuh"
 #include "simt_f32.cuh"
 
 using namespace burst;
@@ -187,6 +188,42 @@ int launch_fwd_bf16(const burst_hop* h, const void* q, const void* k, const void
     fwd::lao_fwd_kernel<D, false><<<grid, fwd::kThreads, fwd::Cfg<D>::kSmemBytes, st>>>(p);
   CHECK_LAUNCH();
   return BURST_OK;
+}
+
+// 64-key-tile forward with double-buffered scores (head_dim 128, dense hops).
+int launch_fwd2_bf16(const burst_hop* h, const void* q, const void* k, const void* v, float* o_acc,
+                     float* m, float* l, void* o_out, float* lse, int first, int fin, cudaStream_t st) {
+  fwd2::Params p;
+  memset(&p, 0, sizeof(p));
+  int rc;
+  if ((rc = make_tmap(&p.tm_q, q, h->n_q, h->heads, 128, h->batch))) return rc;
+  if ((rc = make_tmap(&p.tm_k, k, h->n_k, h->heads, 128, h->batch, 64))) return rc;
+  if ((rc = make_tmap(&p.tm_v, v, h->n_k, h->heads, 128, h->batch, 64))) return rc;
+  p.o_acc = o_acc; p.m_run = m; p.l_run = l; p.o_out = o_out; p.lse_out = lse;
+  p.flags = device_flags();
+  p.hop = *h;
+  p.scale_log2 = h->softmax_scale * kLog2e;
+  p.first_hop = first; p.finalize = fin;
+  static std::once_flag once;
+  static int attr_rc = 0;
+  std::call_once(once, [] { attr_rc = set_smem(fwd2::lao_fwd2_kernel, fwd2::kSmemBytes); });
+  if (attr_rc) return attr_rc;
+  dim3 grid((unsigned)ceil_div(h->q_len, 2 * fwd2::BM), h->heads, h->batch);
+  fwd2::lao_fwd2_kernel<<<grid, fwd2::kThreads, fwd2::kSmemBytes, st>>>(p);
+  CHECK_LAUNCH();
+  return BURST_OK;
+}
+
+// Forward kernel for bf16 head_dim 128 (BURST_FWD_KERNEL / burst_set_fwd_variant:
+// 1 = 128-key tiles (lao_fwd), 2 = 64-key tiles with double-buffered scores (lao_fwd2)).
+std::atomic<int> g_fwd_override{0};
+int fwd_variant() {
+  static int v = [] {
+    const char* e = getenv("BURST_FWD_KERNEL");
+    return (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 1;
+  }();
+  const int o = g_fwd_override.load(std::memory_order_relaxed);
+  return o ? o : v;
 }
 
 template <int D>
@@ -441,7 +478,11 @@ int burst_lao_fwd(const burst_hop* hop, const void* q, const void* k, const void
   if (hop->q_len == 0) return BURST_OK;
   cudaStream_t st = (cudaStream_t)stream;
   if (hop->dtype == BURST_DTYPE_BF16) {
-    if (hop->head_dim == 128) return launch_fwd_bf16<128>(hop, q, k, v, o_acc, m, l, o_out, lse_out, first_hop, finalize, st);
+    if (hop->head_dim == 128) {
+      if (fwd_variant() == 2 && !hop->grid_skip)
+        return launch_fwd2_bf16(hop, q, k, v, o_acc, m, l, o_out, lse_out, first_hop, finalize, st);
+      return launch_fwd_bf16<128>(hop, q, k, v, o_acc, m, l, o_out, lse_out, first_hop, finalize, st);
+    }
     return launch_fwd_bf16<64>(hop, q, k, v, o_acc, m, l, o_out, lse_out, first_hop, finalize, st);
   }
   switch (hop->head_dim) {
@@ -577,6 +618,12 @@ int burst_tl_sum(int dtype, int batch, int heads, int head_dim, int64_t n, const
 int burst_set_bwd_variant(int variant) {
   if (variant < 0 || variant > 6) return fail(BURST_E_SHAPE, "backward variant must be 0 (default) .. 6");
   g_bwd_override.store(variant, std::memory_order_relaxed);
+  return BURST_OK;
+}
+
+int burst_set_fwd_variant(int variant) {
+  if (variant < 0 || variant > 2) return fail(BURST_E_SHAPE, "forward variant must be 0 (default), 1 or 2");
+  g_fwd_override.store(variant, std::memory_order_relaxed);
   return BURST_OK;
 }
 

@@ -260,3 +260,27 @@ def test_backward_variants_parity(bwd_variant, variant, world, causal, zigzag):
     o, lse, dq, dk, dv = oracle_ring(q, k, v, do, world, causal, zigzag)
     for name, got, ref in (("dq", res.dq, dq), ("dk", res.dk, dk), ("dv", res.dv, dv)):
         assert max_abs(got, ref) < BF16_TOL, name
+
+
+@pytest.fixture
+def fwd_variant():
+    from paper_2403_09347_b200 import _lib
+    yield lambda v: _lib.call("burst_set_fwd_variant", v)
+    _lib.call("burst_set_fwd_variant", 0)
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("N,world,causal,zigzag", [(1000, 1, False, False), (1024, 1, True, False),
+                                                   (2048, 4, True, True), (1536, 2, False, False)])
+def test_forward_variants_parity(fwd_variant, variant, N, world, causal, zigzag):
+    """Both bf16 forward kernels (128-key tiles, 64-key tiles with double-buffered
+    scores) against the oracle, including the GAO merge across ring hops."""
+    fwd_variant(variant)
+    q, k, v, do = make_inputs(1, N, 2, 128, seed=N + variant)
+    poison_allocator()
+    res = _run(q, k, v, do, world, causal, zigzag)
+    o, lse, dq, dk, dv = oracle_ring(q, k, v, do, world, causal, zigzag)
+    assert max_abs(res.out, o) < BF16_TOL
+    assert max_abs(res.lse, lse) < 1e-2
+    for name, got, ref in (("dq", res.dq, dq), ("dk", res.dk, dk), ("dv", res.dv, dv)):
+        assert max_abs(got, ref) < BF16_TOL, name
