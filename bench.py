@@ -196,7 +196,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     import torch.distributed as dist
     from paper_2403_09347_b200.api import burst_attn_func
     from paper_2403_09347_b200.kernels import CudaKernels
-    from paper_2403_09347_b200.schedule import hop_flops, plan_hop
+    from paper_2403_09347_b200.schedule import hop_flops
 
     dev = torch.device("cuda", local_rank)
     B, N, H, D, causal = cfg["batch"], cfg["seq"], cfg["heads"], cfg["d"], cfg["causal"]

@@ -53,7 +53,7 @@ def test_nccl_self_exchange_grouped():
 
 
 def test_nccl_rejects_bad_peer():
-    from paper_2403_09347_b200 import NcclError, ShapeError, _lib
+    from paper_2403_09347_b200 import ShapeError, _lib
     lib, h = _one_rank_ring()
     try:
         ops = (_lib.P2POp * 1)()
