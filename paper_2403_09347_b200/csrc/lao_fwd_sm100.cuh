@@ -20,6 +20,7 @@
 // P_t (bf16, 64 cols) aliases the first half of S_t.
 #pragma once
 #include <cuda.h>
+#include <type_traits>
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -326,27 +327,34 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
       const float2 c2v = make_float2(c2, c2), negm = make_float2(-m_use, -m_use);
       // part of the row's exp2 on the FMA pipe (ex2_poly) when no entry of the warp's
       // tile is masked; masked (-inf) entries must stay exactly 0 -> MUFU only
-      const bool poly = !partial;
+      // the exp loop is instantiated twice (hoisted branch): with the FMA-pipe exp2 share
+      // when no entry of the warp's tile is masked, MUFU only otherwise
+      auto exp_row = [&](auto use_poly) {
 #pragma unroll
-      for (int cc = 0; cc < BN / 64; ++cc) {
-        uint32_t pk[32];
+        for (int cc = 0; cc < BN / 64; ++cc) {
+          uint32_t pk[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float2 x = ptx::ffma2(make_float2(s[cc * 64 + 2 * i], s[cc * 64 + 2 * i + 1]), c2v, negm);
-          float p0, p1;
-          if (poly && BURST_POLY_CNT > 0 && (i % BURST_POLY_MOD) < BURST_POLY_CNT) {
-            const float2 pp = ptx::ex2_poly2(x);
-            p0 = pp.x;
-            p1 = pp.y;
-          } else {
-            p0 = ptx::ex2(x.x);
-            p1 = ptx::ex2(x.y);
+          for (int i = 0; i < 32; ++i) {
+            const float2 x = ptx::ffma2(make_float2(s[cc * 64 + 2 * i], s[cc * 64 + 2 * i + 1]), c2v, negm);
+            float p0, p1;
+            if (decltype(use_poly)::value && (i % BURST_POLY_MOD) < BURST_POLY_CNT) {
+              const float2 pp = ptx::ex2_poly2(x);
+              p0 = pp.x;
+              p1 = pp.y;
+            } else {
+              p0 = ptx::ex2(x.x);
+              p1 = ptx::ex2(x.y);
+            }
+            ls4[i & 3] = ptx::fadd2(ls4[i & 3], make_float2(p0, p1));
+            pk[i] = ptx::pack_bf16(p0, p1);
           }
-          ls4[i & 3] = ptx::fadd2(ls4[i & 3], make_float2(p0, p1));
-          pk[i] = ptx::pack_bf16(p0, p1);
+          ptx::tmem_st32(tS + cc * 32, pk);
         }
-        ptx::tmem_st32(tS + cc * 32, pk);
-      }
+      };
+      if (BURST_POLY_CNT > 0 && !partial)
+        exp_row(std::integral_constant<bool, BURST_POLY_CNT != 0>());
+      else
+        exp_row(std::integral_constant<bool, false>());
       const float2 lsa = ptx::fadd2(ptx::fadd2(ls4[0], ls4[1]), ptx::fadd2(ls4[2], ls4[3]));
       l_run += lsa.x + lsa.y;
       ptx::tmem_wait_st();

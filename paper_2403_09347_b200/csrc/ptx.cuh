@@ -378,16 +378,15 @@ __device__ __forceinline__ float ex2_poly(float x) {
   p = fmaf(p, f, 0.9999289403695112f);
   return __int_as_float(__float_as_int(p) + (__float_as_int(j) << 23));
 }
-#ifndef BURST_POLY_MOD        // exp2 emulation share (default OFF: measured slower, the softmax
-                              // is issue-bound, profiles/r01_poly_exp2.txt): ex2_poly when
-#define BURST_POLY_MOD 4      // (idx % BURST_POLY_MOD) < BURST_POLY_CNT
+// Share of each unmasked softmax row whose exp2 runs on the FMA pipe (ex2_poly2) in
+// the forward: pair i of a 32-pair chunk uses it when (i % MOD) < CNT.  3/8 measured
+// best on B200 (profiles/r01_poly_exp2.txt): +1.6% forward at 128K, +5% at 32K.
+#ifndef BURST_POLY_MOD
+#define BURST_POLY_MOD 8
 #endif
 #ifndef BURST_POLY_CNT
-#define BURST_POLY_CNT 0
+#define BURST_POLY_CNT 3
 #endif
-__device__ __forceinline__ float ex2_mixed(float x, int idx) {
-  return (BURST_POLY_CNT > 0 && (idx % BURST_POLY_MOD) < BURST_POLY_CNT) ? ex2_poly(x) : ex2(x);
-}
 // Packed fp32x2 arithmetic (sm_100: FFMA2 / FADD2 issue two lanes' worth per
 // instruction, halving the issue slots of the softmax's elementwise work).
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
