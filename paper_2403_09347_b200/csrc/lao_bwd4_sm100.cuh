@@ -426,13 +426,16 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
       ptx::mbar_wait(ds_empty, (i & 1) ^ 1);
       ptx::tc_fence_after();
       uint8_t* rowp = sdS + hq * 16384 + t * 128;   // SW128 K-major box of this query half
+      // both 32-column halves of this warpgroup's dP^T in one TMEM round trip
+      uint32_t rr[64];
+      ptx::tmem_ld32(tbase + lane_off + kDP + 64 * hq, *reinterpret_cast<uint32_t(*)[32]>(rr));
+      ptx::tmem_ld32(tbase + lane_off + kDP + 64 * hq + 32, *reinterpret_cast<uint32_t(*)[32]>(rr + 32));
+      ptx::tmem_wait_ld();
+      ptx::reg_fence(rr);
+      if (hq == 0) BTRACE4(20, i);
 #pragma unroll
       for (int qc = 0; qc < 2; ++qc) {
-        uint32_t r[32];
-        ptx::tmem_ld32(tbase + lane_off + kDP + 64 * hq + 32 * qc, r);
-        ptx::tmem_wait_ld();
-        ptx::reg_fence(r);
-        if (hq == 0 && qc == 0) BTRACE4(20, i);
+        const uint32_t* r = rr + 32 * qc;
         uint32_t pk[16];
 #pragma unroll
         for (int j4 = 0; j4 < 8; ++j4) {
