@@ -49,7 +49,8 @@ struct Cfg {
   static constexpr int kQuarterBytes = BM * 32 * 4;         // dQ staging: 32 columns
   static constexpr int kPayload = 2 * kTileBytes + 2 * kTileBytes + kTileBytes + kDsBytes +
                                   2 * kQuarterBytes + 2 * kStatBytes;
-  static constexpr int kBarBytes = 128;
+  static constexpr int kLiveWords = 64;    // live-query-tile bitmap (grid masks): 2048 tiles
+  static constexpr int kBarBytes = 128 + 4 * kLiveWords;
   static constexpr int kMaxSmem = 232448;
   static constexpr int kSmemBytes =
       (kPayload + kBarBytes + 1024 <= kMaxSmem) ? kPayload + kBarBytes + 1024 : kMaxSmem;
@@ -154,7 +155,24 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
     const int64_t q0 = qtile(i);
     return grid_rect_live(hp, q0, (q0 + BM < q_end ? q0 + BM : q_end) - q0, k0, krows);
   };
+  // The predicate is evaluated once per tile by the whole CTA into a SMEM bitmap (up to
+  // kLiveWords * 32 tiles); every role then finds the next live tile with __ffs.
+  uint32_t* live_bits = tmem_holder + 2;
+  const bool use_bits = kGrid && nq <= C::kLiveWords * 32;
   auto next_live = [&](int i) -> int {
+    if (!kGrid) return i;
+    if (use_bits) {
+      if (i >= nq) return nq;
+      int w = i >> 5;
+      uint32_t m = live_bits[w] & (~0u << (i & 31));
+      const int nw = (nq + 31) >> 5;
+      while (m == 0u) {
+        if (++w >= nw) return nq;
+        m = live_bits[w];
+      }
+      const int r = (w << 5) + __ffs(m) - 1;
+      return r < nq ? r : nq;
+    }
     while (i < nq && !live(i)) ++i;
     return i;
   };
@@ -188,9 +206,15 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
   }
   if (kGrid) {
     if (threadIdx.x == 0) tmem_holder[1] = 0;
+    if (use_bits)
+      for (int w = threadIdx.x; w < ((nq + 31) >> 5); w += kThreads) live_bits[w] = 0u;
     __syncthreads();
     int mine = 0;
-    for (int i = threadIdx.x; i < nq; i += kThreads) mine += live(i) ? 1 : 0;
+    for (int i = threadIdx.x; i < nq; i += kThreads) {
+      const bool l = live(i);
+      mine += l ? 1 : 0;
+      if (l && use_bits) atomicOr(live_bits + (i >> 5), 1u << (i & 31));
+    }
     mine = __reduce_add_sync(0xffffffffu, mine);
     if (lane == 0 && mine) atomicAdd(tmem_holder + 1, (uint32_t)mine);
   }

@@ -38,7 +38,8 @@ struct Cfg {
   static constexpr int kBoxes = D / 64;
   static constexpr int kTileBytes = kBoxBytes * kBoxes;
   static constexpr int kStages = (D == 128) ? 4 : 6;
-  static constexpr int kSmemBytes = 1024 + 2 * kTileBytes + kStages * kTileBytes + 256;
+  static constexpr int kLiveWords = 256;   // live-KV-tile bitmap (grid masks): 8192 tiles
+  static constexpr int kSmemBytes = 1024 + 2 * kTileBytes + kStages * kTileBytes + 256 + 4 * kLiveWords;
 };
 
 struct Params {
@@ -117,7 +118,32 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
     const int64_t kr = kspan - (int64_t)j * BN;
     return grid_rect_live(hp, row0, qrows, hp.k_begin + (int64_t)j * BN, kr < BN ? kr : BN);
   };
+  // The predicate is evaluated once per tile by the whole CTA into a SMEM bitmap (up to
+  // kLiveWords * 32 tiles); every role then finds the next live tile with __ffs.
+  uint32_t* live_bits = reinterpret_cast<uint32_t*>(bars + 32);
+  const bool use_bits = kGrid && nkv <= C::kLiveWords * 32;
+  if (use_bits) {
+    const int nw = (nkv + 31) >> 5;
+    for (int w = threadIdx.x; w < nw; w += kThreads) live_bits[w] = 0u;
+    __syncthreads();
+    for (int j = threadIdx.x; j < nkv; j += kThreads)
+      if (live(j)) atomicOr(live_bits + (j >> 5), 1u << (j & 31));
+    __syncthreads();
+  }
   auto next_live = [&](int j) -> int {
+    if (!kGrid) return j;
+    if (use_bits) {
+      if (j >= nkv) return nkv;
+      int w = j >> 5;
+      uint32_t m = live_bits[w] & (~0u << (j & 31));
+      const int nw = (nkv + 31) >> 5;
+      while (m == 0u) {
+        if (++w >= nw) return nkv;
+        m = live_bits[w];
+      }
+      const int r = (w << 5) + __ffs(m) - 1;
+      return r < nkv ? r : nkv;
+    }
     while (j < nkv && !live(j)) ++j;
     return j;
   };
