@@ -1,10 +1,10 @@
 // HBM-bound helper kernels around the LAO kernels.
-//   finalize    : O = O_acc / l, lse = (m + log2 l) ln 2   (PartialAttn.finalize,
-//                 local_attn.py:127-135) for rows a causal last hop did not touch
 //   preprocess  : D = rowsum(dO * O) (ring.init_backward, ring.py:207), packed with
 //                 lse*log2e into the backward stats workspace (padded rows -> +inf/0)
-//   bwd_finalize: dQ from its fp32 accumulator; dK/dV = sum of the per-hop
-//                 contributions (sim._collect, sim.py:450-471)
+//   tl_rows     : TL workspace -> row-major output: dQ from its fp32 accumulator,
+//                 dK/dV = sum of the per-hop contributions (sim._collect,
+//                 sim.py:450-471), or the forward finalize O = O_acc / l with lse
+//                 (PartialAttn.finalize, local_attn.py:127-135)
 #pragma once
 #include <cuda_bf16.h>
 #include "common.cuh"
@@ -32,36 +32,6 @@ __device__ __forceinline__ void st4<__nv_bfloat16>(__nv_bfloat16* p, float a, fl
   w.x = *reinterpret_cast<uint32_t*>(&x);
   w.y = *reinterpret_cast<uint32_t*>(&y);
   *reinterpret_cast<uint2*>(p) = w;
-}
-
-// one thread per (b, h, row, 4 columns); consecutive threads = consecutive rows
-// of one TL column group, so TL reads are coalesced.
-template <typename T>
-__global__ void finalize_kernel(int B, int H, int D, int64_t n, const float* __restrict__ o_acc,
-                                const float* __restrict__ m, const float* __restrict__ l,
-                                T* __restrict__ out, float* __restrict__ lse, int* flags) {
-  const int64_t NT = ceil_div(n, 128);
-  const int64_t total = (int64_t)B * H * NT * (D / 4) * 128;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i & 127;
-    int64_t rest = i >> 7;
-    const int c4 = (int)(rest % (D / 4));
-    rest /= (D / 4);
-    const int64_t tile = rest % NT;
-    const int64_t bh = rest / NT;
-    const int64_t row = tile * 128 + r;
-    if (row >= n) continue;
-    const float lv = l[bh * n + row], mv = m[bh * n + row];
-    const float inv = lv > 0.f ? 1.f / lv : 0.f;
-    const float4 o = *reinterpret_cast<const float4*>(o_acc + i * 4);
-    const int64_t b = bh / H, h = bh % H;
-    st4<T>(out + ((b * n + row) * H + h) * D + c4 * 4, o.x * inv, o.y * inv, o.z * inv, o.w * inv);
-    if (c4 == 0) {
-      lse[bh * n + row] = lv > 0.f ? (mv + log2f(lv)) * kLn2 : -INFINITY;
-      if (!(lv > 0.f)) atomicOr(flags, 1);
-    }
-  }
 }
 
 // one warp per (b, h, padded row)
@@ -94,65 +64,55 @@ struct Parts {
   const float* p[16];
 };
 
-template <typename T>
-__global__ void bwd_finalize_kernel(int B, int H, int D, int64_t n, const float* __restrict__ dq_acc,
-                                    Parts dk, Parts dv, int nparts, T* __restrict__ dq,
-                                    T* __restrict__ dko, T* __restrict__ dvo) {
+// TL workspace -> row-major [B, n, H, D] output through a shared-memory transpose.
+// One block per (b*h, 128-row tile, 32-column group): the TL reads are one float4
+// per thread along the tile's rows (coalesced), the output writes are 64-128 B
+// runs along each row (a per-thread row-major store would touch one 8-16 B piece
+// of a different row per thread, 4x write amplification).
+//   kFinal = false: out = sum of the TL parts (dQ from its accumulator, dK/dV from
+//                   the per-hop contributions, sim._collect sim.py:450-471)
+//   kFinal = true : out = O_acc / l and lse = (m + log2 l) ln 2 (PartialAttn.finalize,
+//                   local_attn.py:127-135), parts.p[0] = O_acc
+template <typename T, bool kFinal>
+__global__ void __launch_bounds__(256) tl_rows_kernel(int H, int D, int64_t n, Parts parts, int nparts,
+                                                      T* __restrict__ out, const float* __restrict__ m,
+                                                      const float* __restrict__ l, float* __restrict__ lse,
+                                                      int* flags) {
+  __shared__ float4 s4[128 * 9];   // 128 rows x (8 float4 + 1 pad): conflict-free both ways
+  const int cw = D < 32 ? D : 32, nc4 = cw / 4, ng = D / cw;
   const int64_t NT = ceil_div(n, 128);
-  const int64_t total = (int64_t)B * H * NT * (D / 4) * 128;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i & 127;
-    int64_t rest = i >> 7;
-    const int c4 = (int)(rest % (D / 4));
-    rest /= (D / 4);
-    const int64_t tile = rest % NT;
-    const int64_t bh = rest / NT;
-    const int64_t row = tile * 128 + r;
-    if (row >= n) continue;
-    const int64_t b = bh / H, h = bh % H;
-    const int64_t dst = ((b * n + row) * H + h) * D + c4 * 4;
-    if (dq != nullptr) {
-      const float4 a = *reinterpret_cast<const float4*>(dq_acc + i * 4);
-      st4<T>(dq + dst, a.x, a.y, a.z, a.w);
+  int64_t blk = blockIdx.x;
+  const int cg = (int)(blk % ng);
+  blk /= ng;
+  const int64_t tile = blk % NT, bh = blk / NT;
+  const int64_t base = ((bh * NT + tile) * (D / 4) + cg * nc4) * 128;   // float4 index
+  for (int k = threadIdx.x; k < nc4 * 128; k += 256) {
+    const int c4 = k >> 7, r = k & 127;
+    const int64_t i = base + (int64_t)c4 * 128 + r;
+    float4 a = reinterpret_cast<const float4*>(parts.p[0])[i];
+    for (int j = 1; j < nparts; ++j) {
+      const float4 c = reinterpret_cast<const float4*>(parts.p[j])[i];
+      a.x += c.x; a.y += c.y; a.z += c.z; a.w += c.w;
     }
-    float4 sk = make_float4(0.f, 0.f, 0.f, 0.f), sv = sk;
-    for (int k = 0; k < nparts; ++k) {
-      const float4 a = *reinterpret_cast<const float4*>(dk.p[k] + i * 4);
-      const float4 c = *reinterpret_cast<const float4*>(dv.p[k] + i * 4);
-      sk.x += a.x; sk.y += a.y; sk.z += a.z; sk.w += a.w;
-      sv.x += c.x; sv.y += c.y; sv.z += c.z; sv.w += c.w;
-    }
-    if (nparts > 0) {
-      st4<T>(dko + dst, sk.x, sk.y, sk.z, sk.w);
-      st4<T>(dvo + dst, sv.x, sv.y, sv.z, sv.w);
-    }
+    s4[r * 9 + c4] = a;
   }
-}
-
-// out = sum of TL parts (gradient assembly from per-hop contributions)
-template <typename T>
-__global__ void tl_sum_kernel(int B, int H, int D, int64_t n, Parts parts, int nparts,
-                              T* __restrict__ out) {
-  const int64_t NT = ceil_div(n, 128);
-  const int64_t total = (int64_t)B * H * NT * (D / 4) * 128;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i & 127;
-    int64_t rest = i >> 7;
-    const int c4 = (int)(rest % (D / 4));
-    rest /= (D / 4);
-    const int64_t tile = rest % NT;
-    const int64_t bh = rest / NT;
+  __syncthreads();
+  const int64_t b = bh / H, h = bh % H;
+  for (int k = threadIdx.x; k < nc4 * 128; k += 256) {
+    const int r = k / nc4, g = k % nc4;
     const int64_t row = tile * 128 + r;
     if (row >= n) continue;
-    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int k = 0; k < nparts; ++k) {
-      const float4 a = *reinterpret_cast<const float4*>(parts.p[k] + i * 4);
-      s.x += a.x; s.y += a.y; s.z += a.z; s.w += a.w;
+    float4 v = s4[r * 9 + g];
+    if (kFinal) {
+      const float lv = l[bh * n + row];
+      const float inv = lv > 0.f ? 1.f / lv : 0.f;
+      v.x *= inv; v.y *= inv; v.z *= inv; v.w *= inv;
+      if (cg == 0 && g == 0) {
+        lse[bh * n + row] = lv > 0.f ? (m[bh * n + row] + log2f(lv)) * kLn2 : -INFINITY;
+        if (!(lv > 0.f)) atomicOr(flags, 1);
+      }
     }
-    const int64_t b = bh / H, h = bh % H;
-    st4<T>(out + ((b * n + row) * H + h) * D + c4 * 4, s.x, s.y, s.z, s.w);
+    st4<T>(out + ((b * n + row) * H + h) * D + cg * cw + g * 4, v.x, v.y, v.z, v.w);
   }
 }
 

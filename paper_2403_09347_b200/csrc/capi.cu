@@ -492,19 +492,39 @@ int burst_lao_fwd(const burst_hop* hop, const void* q, const void* k, const void
   }
 }
 
+// TL workspace -> row-major output (aux::tl_rows_kernel), one block per
+// (b*h, 128-row tile, 32-column group).
+static void launch_tl_rows(int dtype, bool final_, int batch, int heads, int head_dim, int64_t n,
+                           const aux::Parts& parts, int nparts, void* out, const float* m,
+                           const float* l, float* lse, cudaStream_t st) {
+  const int cw = head_dim < 32 ? head_dim : 32;
+  const int64_t blocks = (int64_t)batch * heads * ceil_div(n, 128) * (head_dim / cw);
+  if (dtype == BURST_DTYPE_BF16) {
+    if (final_)
+      aux::tl_rows_kernel<__nv_bfloat16, true><<<(unsigned)blocks, 256, 0, st>>>(
+          heads, head_dim, n, parts, nparts, (__nv_bfloat16*)out, m, l, lse, device_flags());
+    else
+      aux::tl_rows_kernel<__nv_bfloat16, false><<<(unsigned)blocks, 256, 0, st>>>(
+          heads, head_dim, n, parts, nparts, (__nv_bfloat16*)out, m, l, lse, device_flags());
+  } else {
+    if (final_)
+      aux::tl_rows_kernel<float, true><<<(unsigned)blocks, 256, 0, st>>>(
+          heads, head_dim, n, parts, nparts, (float*)out, m, l, lse, device_flags());
+    else
+      aux::tl_rows_kernel<float, false><<<(unsigned)blocks, 256, 0, st>>>(
+          heads, head_dim, n, parts, nparts, (float*)out, m, l, lse, device_flags());
+  }
+}
+
 int burst_fwd_finalize(int dtype, int batch, int heads, int head_dim, int64_t n, const float* o_acc,
                        const float* m, const float* l, void* o_out, float* lse_out, void* stream) {
   int rc = check_dims(dtype, batch, heads, head_dim, n);
   if (rc) return rc;
   if (n == 0) return BURST_OK;
-  const int64_t work = (int64_t)burst_workspace_floats(batch, heads, head_dim, n) / 4;
-  cudaStream_t st = (cudaStream_t)stream;
-  if (dtype == BURST_DTYPE_BF16)
-    aux::finalize_kernel<__nv_bfloat16><<<grid_for(work, 256), 256, 0, st>>>(
-        batch, heads, head_dim, n, o_acc, m, l, (__nv_bfloat16*)o_out, lse_out, device_flags());
-  else
-    aux::finalize_kernel<float><<<grid_for(work, 256), 256, 0, st>>>(
-        batch, heads, head_dim, n, o_acc, m, l, (float*)o_out, lse_out, device_flags());
+  aux::Parts pp{};
+  pp.p[0] = o_acc;
+  launch_tl_rows(dtype, true, batch, heads, head_dim, n, pp, 1, o_out, m, l, lse_out,
+                 (cudaStream_t)stream);
   CHECK_LAUNCH();
   return BURST_OK;
 }
@@ -580,16 +600,16 @@ int burst_bwd_finalize(int dtype, int batch, int heads, int head_dim, int64_t n,
     pk.p[i] = i < nparts ? dk_parts[i] : nullptr;
     pv.p[i] = i < nparts ? dv_parts[i] : nullptr;
   }
-  const int64_t work = (int64_t)burst_workspace_floats(batch, heads, head_dim, n) / 4;
   cudaStream_t st = (cudaStream_t)stream;
-  if (dtype == BURST_DTYPE_BF16)
-    aux::bwd_finalize_kernel<__nv_bfloat16><<<grid_for(work, 256), 256, 0, st>>>(
-        batch, heads, head_dim, n, dq_acc, pk, pv, nparts, dq_acc ? (__nv_bfloat16*)dq : nullptr,
-        (__nv_bfloat16*)dk, (__nv_bfloat16*)dv);
-  else
-    aux::bwd_finalize_kernel<float><<<grid_for(work, 256), 256, 0, st>>>(
-        batch, heads, head_dim, n, dq_acc, pk, pv, nparts, dq_acc ? (float*)dq : nullptr, (float*)dk,
-        (float*)dv);
+  if (dq_acc) {
+    aux::Parts pq{};
+    pq.p[0] = dq_acc;
+    launch_tl_rows(dtype, false, batch, heads, head_dim, n, pq, 1, dq, nullptr, nullptr, nullptr, st);
+  }
+  if (nparts > 0) {
+    launch_tl_rows(dtype, false, batch, heads, head_dim, n, pk, nparts, dk, nullptr, nullptr, nullptr, st);
+    launch_tl_rows(dtype, false, batch, heads, head_dim, n, pv, nparts, dv, nullptr, nullptr, nullptr, st);
+  }
   CHECK_LAUNCH();
   return BURST_OK;
 }
@@ -603,14 +623,8 @@ int burst_tl_sum(int dtype, int batch, int heads, int head_dim, int64_t n, const
   if (n == 0) return BURST_OK;
   aux::Parts pp;
   for (int i = 0; i < 16; ++i) pp.p[i] = i < nparts ? parts[i] : nullptr;
-  const int64_t work = (int64_t)burst_workspace_floats(batch, heads, head_dim, n) / 4;
-  cudaStream_t st = (cudaStream_t)stream;
-  if (dtype == BURST_DTYPE_BF16)
-    aux::tl_sum_kernel<__nv_bfloat16><<<grid_for(work, 256), 256, 0, st>>>(
-        batch, heads, head_dim, n, pp, nparts, (__nv_bfloat16*)out);
-  else
-    aux::tl_sum_kernel<float><<<grid_for(work, 256), 256, 0, st>>>(batch, heads, head_dim, n, pp,
-                                                                  nparts, (float*)out);
+  launch_tl_rows(dtype, false, batch, heads, head_dim, n, pp, nparts, out, nullptr, nullptr, nullptr,
+                 (cudaStream_t)stream);
   CHECK_LAUNCH();
   return BURST_OK;
 }
