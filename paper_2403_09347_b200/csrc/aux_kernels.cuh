@@ -20,6 +20,21 @@ template <>
 __device__ __forceinline__ float ld_f<__nv_bfloat16>(const __nv_bfloat16* p) { return __bfloat162float(*p); }
 
 template <typename T>
+__device__ __forceinline__ void ld4(const T* p, float* x);
+template <>
+__device__ __forceinline__ void ld4<float>(const float* p, float* x) {
+  const float4 v = *reinterpret_cast<const float4*>(p);
+  x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+}
+template <>
+__device__ __forceinline__ void ld4<__nv_bfloat16>(const __nv_bfloat16* p, float* x) {
+  const uint2 v = *reinterpret_cast<const uint2*>(p);
+  const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&v.x);
+  const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&v.y);
+  x[0] = __low2float(a); x[1] = __high2float(a); x[2] = __low2float(b); x[3] = __high2float(b);
+}
+
+template <typename T>
 __device__ __forceinline__ void st4(T* p, float a, float b, float c, float d);
 template <>
 __device__ __forceinline__ void st4<float>(float* p, float a, float b, float c, float d) {
@@ -38,7 +53,7 @@ __device__ __forceinline__ void st4<__nv_bfloat16>(__nv_bfloat16* p, float a, fl
 template <typename T>
 __global__ void preprocess_kernel(int B, int H, int D, int64_t n, const T* __restrict__ o,
                                   const T* __restrict__ dout, const float* __restrict__ lse,
-                                  float* __restrict__ stats) {
+                                  float* __restrict__ stats, bool vec) {
   const int64_t NT = ceil_div(n, 128);
   const int64_t rows = (int64_t)B * H * NT * 128;
   const int lane = threadIdx.x & 31;
@@ -49,7 +64,18 @@ __global__ void preprocess_kernel(int B, int H, int D, int64_t n, const T* __res
     if (row < n) {
       const int64_t b = bh / H, h = bh % H;
       const int64_t base = ((b * n + row) * H + h) * D;
-      for (int c = lane; c < D; c += 32) acc = fmaf(ld_f<T>(dout + base + c), ld_f<T>(o + base + c), acc);
+      if (vec) {
+        // 4 consecutive elements per lane (8 B bf16 / 16 B f32 loads)
+        for (int c = lane * 4; c < D; c += 128) {
+          float x[4], y[4];
+          ld4<T>(dout + base + c, x);
+          ld4<T>(o + base + c, y);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc = fmaf(x[e], y[e], acc);
+        }
+      } else {
+        for (int c = lane; c < D; c += 32) acc = fmaf(ld_f<T>(dout + base + c), ld_f<T>(o + base + c), acc);
+      }
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
@@ -86,15 +112,27 @@ __global__ void __launch_bounds__(256) tl_rows_kernel(int H, int D, int64_t n, P
   blk /= ng;
   const int64_t tile = blk % NT, bh = blk / NT;
   const int64_t base = ((bh * NT + tile) * (D / 4) + cg * nc4) * 128;   // float4 index
-  for (int k = threadIdx.x; k < nc4 * 128; k += 256) {
-    const int c4 = k >> 7, r = k & 127;
-    const int64_t i = base + (int64_t)c4 * 128 + r;
-    float4 a = reinterpret_cast<const float4*>(parts.p[0])[i];
-    for (int j = 1; j < nparts; ++j) {
-      const float4 c = reinterpret_cast<const float4*>(parts.p[j])[i];
-      a.x += c.x; a.y += c.y; a.z += c.z; a.w += c.w;
+  // up to 4 float4 per thread (nc4 * 128 <= 1024): all loads of a part in flight at once
+  float4 a[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int k = threadIdx.x + 256 * u;
+    if (k < nc4 * 128) a[u] = reinterpret_cast<const float4*>(parts.p[0])[base + k];
+  }
+  for (int j = 1; j < nparts; ++j) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = threadIdx.x + 256 * u;
+      if (k < nc4 * 128) {
+        const float4 c = reinterpret_cast<const float4*>(parts.p[j])[base + k];
+        a[u].x += c.x; a[u].y += c.y; a[u].z += c.z; a[u].w += c.w;
+      }
     }
-    s4[r * 9 + c4] = a;
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int k = threadIdx.x + 256 * u;   // = c4 * 128 + r
+    if (k < nc4 * 128) s4[(k & 127) * 9 + (k >> 7)] = a[u];
   }
   __syncthreads();
   const int64_t b = bh / H, h = bh % H;

@@ -538,12 +538,15 @@ int burst_bwd_preprocess(int dtype, int batch, int heads, int head_dim, int64_t 
   if (dq_acc) CUDA_TRY(cudaMemsetAsync(dq_acc, 0, ws * sizeof(float), st));
   if (n == 0) return BURST_OK;
   const int64_t rows = (int64_t)batch * heads * ceil_div(n, 128) * 128;
+  // 4-element vector loads when both tensors are aligned to 4 elements
+  const uintptr_t align = dtype == BURST_DTYPE_BF16 ? 8 : 16;
+  const bool vec = (((uintptr_t)o | (uintptr_t)dout) % align) == 0;
   if (dtype == BURST_DTYPE_BF16)
     aux::preprocess_kernel<__nv_bfloat16><<<grid_for(rows * 32, 256), 256, 0, st>>>(
-        batch, heads, head_dim, n, (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, lse, stats);
+        batch, heads, head_dim, n, (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, lse, stats, vec);
   else
     aux::preprocess_kernel<float><<<grid_for(rows * 32, 256), 256, 0, st>>>(
-        batch, heads, head_dim, n, (const float*)o, (const float*)dout, lse, stats);
+        batch, heads, head_dim, n, (const float*)o, (const float*)dout, lse, stats, vec);
   CHECK_LAUNCH();
   return BURST_OK;
 }
