@@ -110,6 +110,23 @@ __device__ __forceinline__ bool grid_rect_live(const burst_hop& h, int64_t q0, i
   return false;
 }
 
+// ... and is every pair of the rectangle outside the skipped cells (no element masking
+// needed inside it)?
+__device__ __forceinline__ bool grid_rect_full(const burst_hop& h, int64_t q0, int64_t nq,
+                                               int64_t k0, int64_t nk) {
+  if (!h.grid_skip || nq <= 0 || nk <= 0) return true;
+  uint32_t ql[2], qh[2], kl[2], kh[2];
+  const uint32_t nkb = (uint32_t)h.grid_nkb;
+  grid_cells_of(h.q_map, q0, nq, (uint32_t)h.grid_qcell, (uint32_t)h.grid_nqb, ql, qh);
+  grid_cells_of(h.k_map, k0, nk, (uint32_t)h.grid_kcell, nkb, kl, kh);
+  for (int a = 0; a < 2; ++a)
+    for (uint32_t qc = ql[a]; qc <= qh[a]; ++qc)
+      for (int b = 0; b < 2; ++b)
+        for (uint32_t kc = kl[b]; kc <= kh[b]; ++kc)
+          if (h.grid_skip[qc * nkb + kc]) return false;
+  return true;
+}
+
 // Tile-interleaved fp32 workspace layout (O_acc, dQ_acc, dK/dV contributions):
 // [B*H][ceil(n/128)][D/4][128 rows][4 cols].  A warp whose lanes own 32
 // consecutive rows touches one contiguous 512 B run per float4 column group,

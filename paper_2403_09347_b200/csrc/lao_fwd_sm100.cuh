@@ -39,7 +39,7 @@ struct Cfg {
   static constexpr int kTileBytes = kBoxBytes * kBoxes;
   static constexpr int kStages = (D == 128) ? 4 : 6;
   static constexpr int kLiveWords = 256;   // live-KV-tile bitmap (grid masks): 8192 tiles
-  static constexpr int kSmemBytes = 1024 + 2 * kTileBytes + kStages * kTileBytes + 256 + 4 * kLiveWords;
+  static constexpr int kSmemBytes = 1024 + 2 * kTileBytes + kStages * kTileBytes + 256 + 8 * kLiveWords;
 };
 
 struct Params {
@@ -119,15 +119,22 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
     return grid_rect_live(hp, row0, qrows, hp.k_begin + (int64_t)j * BN, kr < BN ? kr : BN);
   };
   // The predicate is evaluated once per tile by the whole CTA into a SMEM bitmap (up to
-  // kLiveWords * 32 tiles); every role then finds the next live tile with __ffs.
+  // kLiveWords * 32 tiles); every role then finds the next live tile with __ffs.  A
+  // second bitmap marks tiles lying wholly inside visible cells: the softmax skips the
+  // per-row grid bits there.
   uint32_t* live_bits = reinterpret_cast<uint32_t*>(bars + 32);
+  uint32_t* full_bits = live_bits + C::kLiveWords;
   const bool use_bits = kGrid && nkv <= C::kLiveWords * 32;
   if (use_bits) {
     const int nw = (nkv + 31) >> 5;
-    for (int w = threadIdx.x; w < nw; w += kThreads) live_bits[w] = 0u;
+    for (int w = threadIdx.x; w < nw; w += kThreads) live_bits[w] = full_bits[w] = 0u;
     __syncthreads();
-    for (int j = threadIdx.x; j < nkv; j += kThreads)
+    for (int j = threadIdx.x; j < nkv; j += kThreads) {
       if (live(j)) atomicOr(live_bits + (j >> 5), 1u << (j & 31));
+      const int64_t kr = kspan - (int64_t)j * BN;
+      if (grid_rect_full(hp, row0, qrows, hp.k_begin + (int64_t)j * BN, kr < BN ? kr : BN))
+        atomicOr(full_bits + (j >> 5), 1u << (j & 31));
+    }
     __syncthreads();
   }
   auto next_live = [&](int j) -> int {
@@ -292,6 +299,15 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
     float m_run = -INFINITY, l_run = 0.f;
 
     for (int j = first, jj = 0; j < nkv; j = next_live(j + 1), ++jj) {
+      const int64_t nvalid = lim - (int64_t)j * BN;
+      uint64_t gk0 = 0, gk1 = 0;   // block-sparse grid: hidden key columns of this row
+      if (kGrid && !(use_bits && ((full_bits[j >> 5] >> (j & 31)) & 1u))) {
+        // (computed before the S wait so the table lookups overlap the MMA)
+        const int nv = nvalid > BN ? BN : (nvalid < 0 ? 0 : (int)nvalid);
+        const int64_t kt0 = hp.k_begin + (int64_t)j * BN;
+        if (nv > 0) gk0 = grid_key_bits(hp, qpos, kt0, nv < 64 ? nv : 64);
+        if (nv > 64) gk1 = grid_key_bits(hp, qpos, kt0 + 64, nv - 64);
+      }
       ptx::mbar_wait(s_full + g, jj & 1); FTRACE(3 + 8 * g, jj);
       ptx::tc_fence_after();
       float s[BN];
@@ -304,14 +320,6 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
         ptx::reg_fence(r);
 #pragma unroll
         for (int i = 0; i < BN; ++i) s[i] = __uint_as_float(r[i]);
-      }
-      const int64_t nvalid = lim - (int64_t)j * BN;
-      uint64_t gk0 = 0, gk1 = 0;   // block-sparse grid: hidden key columns of this row
-      if (kGrid) {
-        const int nv = nvalid > BN ? BN : (nvalid < 0 ? 0 : (int)nvalid);
-        const int64_t kt0 = hp.k_begin + (int64_t)j * BN;
-        if (nv > 0) gk0 = grid_key_bits(hp, qpos, kt0, nv < 64 ? nv : 64);
-        if (nv > 64) gk1 = grid_key_bits(hp, qpos, kt0 + 64, nv - 64);
       }
       const bool partial = __any_sync(0xffffffffu, nvalid < BN || (gk0 | gk1) != 0);
       if (partial) {
