@@ -326,9 +326,10 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     # ---- e2e through the public API with pinned host buffers, as a training loop
     # would run it: step i's inputs are copied host->device while step i-1 computes
-    # and step i's results go device->host while step i+1 computes (one stream per
-    # copy direction, double-buffered device inputs).  The timed region starts
-    # before the first H2D and ends after the last D2H.
+    # (dO may still be in flight during step i's forward) and step i's results go
+    # device->host while step i+1 computes (O already during step i's backward; one
+    # stream per copy direction, double-buffered device inputs).  The timed region
+    # starts before the first H2D and ends after the last D2H.
     host = [t.detach().cpu().pin_memory() for t in (q, k, v, do)]
     outs = [torch.empty(B, n, H, D, dtype=torch.bfloat16).pin_memory() for _ in range(4)]
     dbuf = [[torch.empty(B, n, H, D, device=dev, dtype=torch.bfloat16) for _ in range(4)]
@@ -337,7 +338,9 @@ def run_ours(args, cfg, rank, world, local_rank):
     h2d, d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
 
     def run_e2e(nsteps, e_start=None, e_stop=None):
-        ev_in = [torch.cuda.Event(), torch.cuda.Event()]
+        # per buffer: q/k/v landed (the forward may start), dO landed (the backward may)
+        ev_qkv = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_do = [torch.cuda.Event(), torch.cuda.Event()]
         ev_done = [None, None]
         if e_start is not None:
             e_start.record(h2d)
@@ -347,16 +350,27 @@ def run_ours(args, cfg, rank, world, local_rank):
             if ev_done[i % 2] is not None:
                 h2d.wait_event(ev_done[i % 2])     # step i-2 has finished reading b
             with torch.cuda.stream(h2d):
-                for dst, src in zip(b, host):
+                for dst, src in zip(b[:3], host[:3]):
                     dst.copy_(src, non_blocking=True)
-            ev_in[i % 2].record(h2d)
+                ev_qkv[i % 2].record(h2d)
+                b[3].copy_(host[3], non_blocking=True)
+                ev_do[i % 2].record(h2d)
 
         load(0)
         for i in range(nsteps):
-            comp.wait_event(ev_in[i % 2])
+            comp.wait_event(ev_qkv[i % 2])
             qq, kk, vv, dd = dbuf[i % 2]
             qq, kk, vv = (x.detach().requires_grad_(True) for x in (qq, kk, vv))
-            o, (gq, gk, gv) = step(qq, kk, vv, dd)
+            o, lse = burst_attn_func(qq, kk, vv, causal=causal, zigzag=zigzag, _kernels=kern,
+                                     comm=args.comm, mask=cfg.get("mask"))
+            fwd_done = torch.cuda.Event()
+            fwd_done.record(comp)
+            d2h.wait_event(fwd_done)               # O leaves while the backward runs
+            with torch.cuda.stream(d2h):
+                o.record_stream(d2h)
+                outs[0].copy_(o.detach(), non_blocking=True)
+            comp.wait_event(ev_do[i % 2])
+            gq, gk, gv = torch.autograd.grad(o, (qq, kk, vv), dd)
             done = torch.cuda.Event()
             done.record(comp)
             ev_done[i % 2] = done
@@ -364,7 +378,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                 load(i + 1)
             d2h.wait_event(done)
             with torch.cuda.stream(d2h):
-                for dst, src in zip(outs, (o, gq, gk, gv)):
+                for dst, src in zip(outs[1:], (gq, gk, gv)):
                     src.record_stream(d2h)
                     dst.copy_(src.detach(), non_blocking=True)
         if e_stop is not None:
@@ -446,7 +460,9 @@ def run_ours(args, cfg, rank, world, local_rank):
                 "h2d_bytes_per_step": 4 * tensor_bytes, "d2h_bytes_per_step": 4 * tensor_bytes,
                 "ms_per_step": e2e_ms, "steps": e2e_steps,
                 "api": "burst_attn_func + autograd; pinned host buffers, H2D of step i+1 and "
-                       "D2H of step i on two copy streams overlapping step i's compute"},
+                       "D2H of step i on two copy streams overlapping compute (dO lands during "
+                       "the forward, O leaves during the backward); window includes the "
+                       "pipeline fill and drain"},
         "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary(),
         "gpu_launches": launches, "comm": comm,
     }
