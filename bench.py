@@ -243,9 +243,14 @@ def run_ours(args, cfg, rank, world, local_rank):
             self.launches += 1
             return super().bwd_prepare(*a, **kw)
 
-        def bwd_finalize(self, *a, **kw):
+        def tl_sum(self, *a, **kw):
             self.launches += 1
-            return super().bwd_finalize(*a, **kw)
+            return super().tl_sum(*a, **kw)
+
+        def bwd_finalize(self, st, dk_parts, *a, **kw):
+            # burst_bwd_finalize = one tl_rows launch for dQ + one each for dK, dV
+            self.launches += 3 if dk_parts else 1
+            return super().bwd_finalize(st, dk_parts, *a, **kw)
 
     kern = TimedKernels()
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
