@@ -30,6 +30,10 @@ namespace fwd {
 constexpr int BM = 128;       // query rows per tile
 constexpr int BN = 128;       // keys per tile
 constexpr int kThreads = 384;   // 3 warpgroups (warps 10-11 idle) for setmaxnreg
+#ifndef BURST_FWD_PSPLIT   // key chunks of P handed to the O += P V MMAs one at a time
+#define BURST_FWD_PSPLIT 2
+#endif
+constexpr int kPS = BURST_FWD_PSPLIT;        // 1, 2 or 4
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: lazy rescale (values <= 2^8)
 
 template <int D>
@@ -87,8 +91,8 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
   uint64_t* kv_full = bars + 1;
   uint64_t* kv_empty = kv_full + C::kStages;
   uint64_t* s_full = kv_empty + C::kStages;   // [2]
-  uint64_t* p_full = s_full + 2;              // [2]
-  uint64_t* o_full = p_full + 2;
+  uint64_t* p_full = s_full + 2;              // [2 tiles][kPS key chunks]
+  uint64_t* o_full = p_full + 2 * kPS;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_full + 1);
 
   const burst_hop& hp = p.hop;
@@ -166,7 +170,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
       }
       for (int t = 0; t < 2; ++t) {
         ptx::mbar_init(s_full + t, 1);
-        ptx::mbar_init(p_full + t, BM);
+        for (int c = 0; c < kPS; ++c) ptx::mbar_init(p_full + kPS * t + c, BM);
       }
       ptx::mbar_init(o_full, 1);
       ptx::fence_mbar_init();
@@ -229,13 +233,17 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
         }
         __syncwarp();
       };
-      auto pv = [&](int t, int slot, bool acc) {
+      // O_t += P_t V in kPS key chunks: a chunk's MMAs start as soon as the softmax has
+      // stored its P, overlapping the exp2 of the following keys
+      auto pv = [&](int t, int slot, bool acc, int chunk) {
         if (ptx::elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BN / 16; ++kk)
+          for (int k4 = 0; k4 < BN / 16 / kPS; ++k4) {
+            const int kk = chunk * (BN / 16 / kPS) + k4;
             ptx::mma_ts(tbase + 256 + t * D, tbase + t * 128 + kk * 8,
                         dKVm + slot * kTile + (uint64_t)(kk * 2048 >> 4), idesc_pv,
                         (acc || kk > 0) ? 1u : 0u);
+          }
         }
         __syncwarp();
       };
@@ -256,17 +264,21 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
         const int itk = 2 * jj + 2, sk = itk % C::kStages;
         const bool more = jn < nkv;
         ptx::mbar_wait(kv_full + sv, (itv / C::kStages) & 1); FTRACE(0, jj);
-        ptx::mbar_wait(p_full + 0, jj & 1); FTRACE(1, jj);
-        ptx::tc_fence_after();
-        pv(0, sv, jj > 0);
+        for (int c = 0; c < kPS; ++c) {
+          ptx::mbar_wait(p_full + c, jj & 1); if (c == 0) FTRACE(1, jj);
+          ptx::tc_fence_after();
+          pv(0, sv, jj > 0, c);
+        }
         if (more) {
           ptx::mbar_wait(kv_full + sk, (itk / C::kStages) & 1);
           ptx::tc_fence_after();
           qk(0, sk);
         }
-        ptx::mbar_wait(p_full + 1, jj & 1); FTRACE(2, jj);
-        ptx::tc_fence_after();
-        pv(1, sv, jj > 0);
+        for (int c = 0; c < kPS; ++c) {
+          ptx::mbar_wait(p_full + kPS + c, jj & 1); if (c == 0) FTRACE(2, jj);
+          ptx::tc_fence_after();
+          pv(1, sv, jj > 0, c);
+        }
         commit(kv_empty + sv);
         if (more) {
           qk(1, sk);
@@ -365,11 +377,13 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
       // when no entry of the warp's tile is masked, MUFU only otherwise
       auto exp_row = [&](auto use_poly) {
 #pragma unroll
-        for (int cc = 0; cc < BN / 64; ++cc) {
-          uint32_t pk[32];
+        for (int cc = 0; cc < kPS; ++cc) {
+          constexpr int kPairs = BN / 2 / kPS;
+          uint32_t pk[kPairs];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float2 x = ptx::ffma2(make_float2(s[cc * 64 + 2 * i], s[cc * 64 + 2 * i + 1]), c2v, negm);
+          for (int i = 0; i < kPairs; ++i) {
+            const float2 x = ptx::ffma2(make_float2(s[cc * 2 * kPairs + 2 * i], s[cc * 2 * kPairs + 2 * i + 1]),
+                                        c2v, negm);
             float p0, p1;
             if (decltype(use_poly)::value && (i % BURST_POLY_MOD) < BURST_POLY_CNT) {
               const float2 pp = ptx::ex2_poly2(x);
@@ -382,7 +396,18 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
             ls4[i & 3] = ptx::fadd2(ls4[i & 3], make_float2(p0, p1));
             pk[i] = ptx::pack_bf16(p0, p1);
           }
-          ptx::tmem_st32(tS + cc * 32, pk);
+          if constexpr (kPairs == 64) {
+            ptx::tmem_st32(tS, *reinterpret_cast<const uint32_t(*)[32]>(pk));
+            ptx::tmem_st32(tS + 32, *reinterpret_cast<const uint32_t(*)[32]>(pk + 32));
+          } else if constexpr (kPairs == 32) {
+            ptx::tmem_st32(tS + cc * 32, *reinterpret_cast<const uint32_t(*)[32]>(pk));
+          } else {
+            ptx::tmem_st16(tS + cc * 16, *reinterpret_cast<const uint32_t(*)[16]>(pk));
+          }
+          // P for this key chunk is in TMEM: its O += P V MMAs may start
+          ptx::tmem_wait_st();
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(p_full + kPS * g + cc);
         }
       };
       if (BURST_POLY_CNT > 0 && !partial)
@@ -391,9 +416,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
         exp_row(std::integral_constant<bool, false>());
       const float2 lsa = ptx::fadd2(ptx::fadd2(ls4[0], ls4[1]), ptx::fadd2(ls4[2], ls4[3]));
       l_run += lsa.x + lsa.y;
-      ptx::tmem_wait_st();
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(p_full + g); FTRACE(5 + 8 * g, jj);
+      FTRACE(5 + 8 * g, jj);
     }
 
     // ------------------------------------------------------------ epilogue
