@@ -80,11 +80,25 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200", "-i", str(self.gpu)], stdout=open(self.path, "w"),
+                 "-lms", "100", "-i", str(self.gpu)], stdout=open(self.path, "w"),
                 stderr=subprocess.DEVNULL)
         except Exception:  # noqa: BLE001
             self.proc = None
+        # nvidia-smi needs ~0.5-1 s before its first sample: wait for it so short timed
+        # regions (C2: ~0.3 s) are sampled; rows before the region are dropped below
+        t0 = time.time()
+        while self.proc is not None and time.time() - t0 < 5.0:
+            if self._lines():
+                break
+            time.sleep(0.05)
+        self.skip = len(self._lines())
         return self
+
+    def _lines(self):
+        try:
+            return [ln for ln in open(self.path) if ln.strip()]
+        except Exception:  # noqa: BLE001
+            return []
 
     def __exit__(self, *a):
         if self.proc is not None:
@@ -93,13 +107,10 @@ class ClockSampler:
 
     def summary(self):
         rows = []
-        try:
-            for line in open(self.path):
-                f = [x.strip() for x in line.split(",")]
-                if len(f) >= 9 and f[1].replace(".", "").isdigit():
-                    rows.append(f)
-        except Exception:  # noqa: BLE001
-            pass
+        for line in self._lines()[getattr(self, "skip", 0):]:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9 and f[1].replace(".", "").isdigit():
+                rows.append(f)
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         sm = [float(r[1]) for r in rows]
