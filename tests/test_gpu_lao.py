@@ -59,6 +59,24 @@ def test_ring_bf16_loopback(world, causal, zigzag):
         assert max_abs(got, ref) < BF16_TOL
 
 
+@pytest.mark.parametrize("B,H,N,D,world,causal,zigzag", [
+    (2, 3, 1536, 128, 2, True, True),     # batch x heads > 1 through a zigzag ring
+    (3, 2, 1024, 64, 4, False, False),    # head_dim 64 bf16 ring
+    (2, 1, 2304, 128, 2, False, False),   # shard of 1152 rows: partial last query/key tiles
+])
+def test_ring_bf16_batched(B, H, N, D, world, causal, zigzag):
+    """Batch and head indexing of every kernel (TMA coordinates, TL workspaces, stats)
+    through the ring, including head_dim 64 and shards that are not tile multiples."""
+    q, k, v, do = make_inputs(B, N, H, D, seed=B * 100 + H * 10 + world)
+    poison_allocator()
+    res = _run(q, k, v, do, world, causal, zigzag)
+    o, lse, dq, dk, dv = oracle_ring(q, k, v, do, world, causal, zigzag)
+    assert max_abs(res.out, o) < BF16_TOL
+    assert max_abs(res.lse, lse) < 1e-2
+    for name, got, ref in (("dq", res.dq, dq), ("dk", res.dk, dk), ("dv", res.dv, dv)):
+        assert max_abs(got, ref) < BF16_TOL, name
+
+
 @pytest.mark.parametrize("N,D,world,causal", [(512, 64, 1, False), (512, 32, 2, True),
                                               (300, 16, 1, True)])
 def test_f32_path_rel_1e5(N, D, world, causal):
