@@ -67,3 +67,31 @@ def test_lao_rectangle_with_global_offsets():
         ro, rl = part.finalize()
         assert max_abs(o[0, :, h], ro) < 2e-2
         assert max_abs(lse[0, h], rl) < 1e-2
+
+
+def test_integration_stub_runs_on_gpu():
+    """The raw-ctypes binding of INTEGRATION.md (what a maintainer adds to the reference)
+    computes one offset causal rectangle like the oracle's local_forward_tiled."""
+    import os
+    from oracle import burst_oracle as orc
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    doc = open(os.path.join(root, "INTEGRATION.md")).read()
+    sec = doc[doc.index("## Reference-side binding"):]
+    code = sec[sec.index("```python") + len("```python"):]
+    code = code[:code.index("```")]
+    lib_path = os.path.join(root, "paper_2403_09347_b200", "libburst_b200.so")
+    ns = {}
+    exec(compile(code.replace('"libburst_b200.so"', repr(lib_path)), "INTEGRATION.md", "exec"), ns)
+    B, H, D, n_q, n_k, r0, c0 = 1, 2, 128, 256, 384, 512, 256
+    q, _, _, _ = make_inputs(B, n_q, H, D, seed=21)
+    _, k, v, _ = make_inputs(B, n_k, H, D, seed=22)
+    scale = D ** -0.5
+    out, lse = ns["local_forward_b200"](q, k, v, scale, row_offset=r0, col_offset=c0, causal=True)
+    torch.cuda.synchronize()
+    for h in range(H):
+        f = lambda t: t[0, :, h].float().cpu().numpy().astype(np.float64)
+        part = orc.local_forward_tiled(f(q), f(k), f(v), scale, 128, 128,
+                                       np.arange(r0, r0 + n_q), np.arange(c0, c0 + n_k), True)
+        ro, rl = part.finalize()
+        assert np.abs(out[0, :, h].float().cpu().numpy() - ro).max() < 2e-2
+        assert np.abs(lse[0, h].cpu().numpy() - rl).max() < 1e-2

@@ -60,6 +60,27 @@ int main(void) {
     assert got == want
 
 
+def test_integration_stub():
+    """The raw-ctypes binding printed in INTEGRATION.md loads the library and declares
+    burst_hop / burst_posmap exactly as the C header lays them out."""
+    from paper_2403_09347_b200 import _lib
+    import ctypes
+    doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    sec = doc[doc.index("## Reference-side binding"):]
+    code = sec[sec.index("```python") + len("```python"):]
+    code = code[:code.index("```")]
+    lib_path = os.path.join(ROOT, "paper_2403_09347_b200", "libburst_b200.so")
+    assert 'ctypes.CDLL("libburst_b200.so")' in code
+    ns = {}
+    exec(compile(code.replace('"libburst_b200.so"', repr(lib_path)), "INTEGRATION.md", "exec"), ns)
+    for mine, ref in ((ns["Hop"], _lib.Hop), (ns["PosMap"], _lib.PosMap)):
+        assert ctypes.sizeof(mine) == ctypes.sizeof(ref)
+        assert [(f[0], getattr(mine, f[0]).offset) for f in mine._fields_] == \
+               [(f[0], getattr(ref, f[0]).offset) for f in ref._fields_]
+    assert len(ns["_lib"].burst_lao_fwd.argtypes) == len(_lib._SIGS["burst_lao_fwd"][0])
+    assert callable(ns["local_forward_b200"])
+
+
 def test_errors_map_to_reference_taxonomy():
     from paper_2403_09347_b200 import errors
     assert errors.CODE_TO_ERROR[1] is errors.ShapeError
