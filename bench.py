@@ -425,10 +425,11 @@ def run_ours(args, cfg, rank, world, local_rank):
     peak_src = "MEASURED_PEAKS.json" if peaks else "fallback (B200_PROFILING.md)"
     tokens = B * N / (ms / 1e3)
     tflops_gpu = _flops(cfg) / world / (ms / 1e3) / 1e12
-    traffic = None
+    traffic = traffic_fwd = None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
         traffic = tr.get(f"{args.config}_g{world}", {}).get("lao_bwd")
+        traffic_fwd = tr.get(f"{args.config}_g{world}", {}).get("lao_fwd")
     except Exception:  # noqa: BLE001
         pass
     roof = None
@@ -443,7 +444,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             fa = fwd_fl / (fwd_ms / 1e3) / 1e12
             roof["lao_fwd"] = {"achieved": fa, "frac": fa / peak_sus,
                                "frac_of_burst_peak": fa / peak_burst, "ms_per_launch": fwd_ms,
-                               "flops_per_launch": fwd_fl}
+                               "flops_per_launch": fwd_fl, "traffic": traffic_fwd}
     cpu = None
     if world == 1 and not args.skip_cpu:
         dt, factor = cpu_reference_sample(cfg, 1, args.ref_rows)
