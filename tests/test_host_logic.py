@@ -382,3 +382,25 @@ def test_grid_mask_from_spec_file(tmp_path):
     assert causal and g.n_query_blocks == 2 and g.skip == frozenset({(1, 0)})
     assert GridMask.from_spec("causal") == (None, True)
     assert GridMask.from_spec(None) == (None, False)
+
+
+# ---------------------------------------------------------------- bench reference arm
+
+def test_bench_reference_arm_cpu():
+    """`bench.py --impl reference` (the driver's reference arm: the reference algorithm on
+    the host cores) prints one JSON line with the contract's keys; under torchrun only
+    rank 0 prints."""
+    import json
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "c2",
+           "--steps", "1", "--warmup", "0", "--ref-rows", "32"]
+    env = dict(os.environ, RANK="0", WORLD_SIZE="1")
+    out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["unit"] == "tokens/s" and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "port" and d["e2e"]["h2d_bytes_per_step"] == 0
+    env = dict(os.environ, RANK="1", WORLD_SIZE="2")
+    out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=300)
+    assert out.returncode == 0 and not out.stdout.strip()
