@@ -379,13 +379,13 @@ __device__ __forceinline__ float ex2_poly(float x) {
   return __int_as_float(__float_as_int(p) + (__float_as_int(j) << 23));
 }
 // Share of each unmasked softmax row whose exp2 runs on the FMA pipe (ex2_poly2) in
-// the forward: pair i of a 32-pair chunk uses it when (i % MOD) < CNT.  3/8 measured
-// best on B200 (profiles/r01_poly_exp2.txt): +1.6% forward at 128K, +5% at 32K.
+// the forward: pair i of a 32-pair chunk uses it when (i % MOD) < CNT.  5/16 measured
+// best on B200 with P handed over in key halves (profiles/r01_poly_exp2.txt; 3/8 before).
 #ifndef BURST_POLY_MOD
-#define BURST_POLY_MOD 8
+#define BURST_POLY_MOD 16
 #endif
 #ifndef BURST_POLY_CNT
-#define BURST_POLY_CNT 3
+#define BURST_POLY_CNT 5
 #endif
 // Packed fp32x2 arithmetic (sm_100: FFMA2 / FADD2 issue two lanes' worth per
 // instruction, halving the issue slots of the softmax's elementwise work).
