@@ -82,6 +82,10 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
 template <int D, bool kGrid>
 __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_constant__ Params p) {
   using C = Cfg<D>;
+  // FMA-pipe exp2 share (profiles/r01_poly_exp2.txt): 5/16 measured best for dense hops,
+  // 3/8 for the grid-masked instantiation (c3_sparse: 122.5 vs 126.3 ms per launch)
+  constexpr int kPolyMod = kGrid ? 8 : BURST_POLY_MOD;
+  constexpr int kPolyCnt = kGrid ? 3 : BURST_POLY_CNT;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* sQ = smem;                          // 2 tiles
@@ -385,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
             const float2 x = ptx::ffma2(make_float2(s[cc * 2 * kPairs + 2 * i], s[cc * 2 * kPairs + 2 * i + 1]),
                                         c2v, negm);
             float p0, p1;
-            if (decltype(use_poly)::value && (i % BURST_POLY_MOD) < BURST_POLY_CNT) {
+            if (decltype(use_poly)::value && (i % kPolyMod) < kPolyCnt) {
               const float2 pp = ptx::ex2_poly2(x);
               p0 = pp.x;
               p1 = pp.y;
@@ -410,8 +414,8 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
           ptx::mbar_arrive(p_full + kPS * g + cc);
         }
       };
-      if (BURST_POLY_CNT > 0 && !partial)
-        exp_row(std::integral_constant<bool, BURST_POLY_CNT != 0>());
+      if (kPolyCnt > 0 && !partial)
+        exp_row(std::integral_constant<bool, kPolyCnt != 0>());
       else
         exp_row(std::integral_constant<bool, false>());
       const float2 lsa = ptx::fadd2(ptx::fadd2(ls4[0], ls4[1]), ptx::fadd2(ls4[2], ls4[3]));
