@@ -258,6 +258,14 @@ def run_ours(args, cfg, rank, world, local_rank):
             self.launches += 1
             return super().tl_sum(*a, **kw)
 
+        def accumulate(self, *a, **kw):
+            self.launches += 2          # one burst_tl_accumulate per dK, dV buffer
+            return super().accumulate(*a, **kw)
+
+        def accumulate_dq(self, *a, **kw):
+            self.launches += 1
+            return super().accumulate_dq(*a, **kw)
+
         def bwd_finalize(self, st, dk_parts, *a, **kw):
             # burst_bwd_finalize = one tl_rows launch for dQ + one each for dK, dV
             self.launches += 3 if dk_parts else 1

@@ -16,6 +16,7 @@
  *                        = ring.backward_step accumulation (ring.py:221-242)
  *   burst_bwd_finalize   sim._collect gradient assembly    (sim.py:450-471)
  *   burst_tl_sum         same, for travelling-query dQ contributions (ring.py:65-83)
+ *   burst_tl_accumulate  in-place accumulation of a received contribution (ring.py:239-241)
  *   burst_ring_*         sim.RingChannel send/recv, DoubleBuffer (sim.py:281-332)
  *   burst_ipc_*, burst_copy_async, burst_event_* / burst_stream_wait_event
  *                        the same hand-off over copy engines (zero SM), SURVEY f1
@@ -81,6 +82,11 @@ typedef struct {
   const uint8_t* grid_skip;
   int32_t grid_nqb, grid_nkb;
   int64_t grid_qcell, grid_kcell;
+  /* Device int32 error word of the pass this hop belongs to (NULL = the per-device
+   * default word of burst_read_flags).  Kernels OR in bit 0 (a row with no visible
+   * key -> MaskError), bit 1 (non-finite output -> NonFiniteError), bit 2 (launch
+   * could not run -> CudaError). */
+  int32_t* flags;
 } burst_hop;
 
 /* Elements (float) of one TL workspace for [batch, n, heads, head_dim]. */
@@ -93,10 +99,11 @@ BURST_API int burst_lao_fwd(const burst_hop* hop, const void* q, const void* k, 
                   float* m, float* l, void* o_out, float* lse_out, int first_hop, int finalize,
                   void* stream);
 
-/* Normalise a running state: o_out = o_acc / l, lse = ln-domain(m, l). */
+/* Normalise a running state: o_out = o_acc / l, lse = ln-domain(m, l).  `flags`:
+ * error word (see burst_hop.flags; NULL = per-device default). */
 BURST_API int burst_fwd_finalize(int dtype, int batch, int heads, int head_dim, int64_t n,
                        const float* o_acc, const float* m, const float* l, void* o_out,
-                       float* lse_out, void* stream);
+                       float* lse_out, int32_t* flags, void* stream);
 
 /* Backward stats for every (b, h, row) of a [batch, n] query block, packed as
  * stats[0][B*H][ceil(n/128)*128] = lse * log2(e) and stats[1][...] = D =
@@ -114,27 +121,27 @@ BURST_API int burst_lao_bwd(const burst_hop* hop, const void* q, const void* k, 
                   const void* dout, const float* stats, float* dq_acc, float* dk_acc,
                   float* dv_acc, int accumulate, void* stream);
 
-/* dq = dq_acc; dk = sum of nparts dk partials; dv likewise (TL f32 -> dtype). */
+/* dq = dq_acc; dk = sum of nparts (1..16) dk partials; dv likewise (TL f32 -> dtype).
+ * Outputs are checked for non-finite values (flags bit 1). */
 BURST_API int burst_bwd_finalize(int dtype, int batch, int heads, int head_dim, int64_t n,
                        const float* dq_acc, const float* const* dk_parts,
                        const float* const* dv_parts, int nparts, void* dq, void* dk, void* dv,
-                       void* stream);
+                       int32_t* flags, void* stream);
 
 /* out = sum of nparts TL f32 buffers (TL f32 -> dtype [batch, n, heads, head_dim]).
  * Assembles a gradient from per-hop contributions: the dQ contributions of the
  * reference's travelling-query backward payload (ring.py:65-83, 221-242; sim._collect
  * sim.py:450-471) when K/V/dK/dV stay pinned. */
 BURST_API int burst_tl_sum(int dtype, int batch, int heads, int head_dim, int64_t n,
-                 const float* const* parts, int nparts, void* out, void* stream);
+                 const float* const* parts, int nparts, void* out, int32_t* flags,
+                 void* stream);
 
-/* Select the bf16 head_dim-128 backward kernel for later burst_lao_bwd calls:
- * 0 = default (BURST_BWD_KERNEL env or 4), 1 = lao_bwd, 3 = bwd3, 4 = bwd4 (default),
- * 5 (or 2) = bwd5 (CTA pair, dS^T in TMEM).  Process-wide. */
-BURST_API int burst_set_bwd_variant(int variant);
-
-/* Select the bf16 head_dim-128 forward kernel: 0 = default (BURST_FWD_KERNEL env or 1),
- * 1 = 128-key tiles, 2 = 64-key tiles with double-buffered scores (dense hops only). */
-BURST_API int burst_set_fwd_variant(int variant);
+/* acc += part over one TL workspace of [batch, n, heads, head_dim] (both f32 TL).
+ * Folds a received dK/dV (or dQ) contribution into the home accumulator as soon as
+ * its exchange has landed, so a rank holds O(1) contribution buffers for any ring
+ * size (the in-place accumulation of ring.backward_step, ring.py:239-241). */
+BURST_API int burst_tl_accumulate(int batch, int heads, int head_dim, int64_t n, float* acc,
+                        const float* part, void* stream);
 
 /* Non-zero device-side flags raised by kernels since the last call (bit 0: a
  * row with no visible key, bit 1: non-finite output).  Synchronises `stream`. */

@@ -36,7 +36,7 @@ class Hop(ctypes.Structure):
                 ("softmax_scale", _c_f32), ("causal", _c_i32),
                 ("q_map", PosMap), ("k_map", PosMap),
                 ("grid_skip", _c_p), ("grid_nqb", _c_i32), ("grid_nkb", _c_i32),
-                ("grid_qcell", _c_i64), ("grid_kcell", _c_i64)]
+                ("grid_qcell", _c_i64), ("grid_kcell", _c_i64), ("flags", _c_p)]
 
 
 class P2POp(ctypes.Structure):
@@ -51,19 +51,18 @@ _SIGS = {
     "burst_lao_fwd": ([ctypes.POINTER(Hop), _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
                        _c_i32, _c_i32, _c_p], _c_i32),
     "burst_fwd_finalize": ([_c_i32, _c_i32, _c_i32, _c_i32, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p,
-                            _c_p], _c_i32),
+                            _c_p, _c_p], _c_i32),
     "burst_bwd_preprocess": ([_c_i32, _c_i32, _c_i32, _c_i32, _c_i64, _c_p, _c_p, _c_p, _c_p,
                               _c_p, _c_p], _c_i32),
     "burst_lao_bwd": ([ctypes.POINTER(Hop), _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
                        _c_i32, _c_p], _c_i32),
     "burst_bwd_finalize": ([_c_i32, _c_i32, _c_i32, _c_i32, _c_i64, _c_p,
                             ctypes.POINTER(_c_p), ctypes.POINTER(_c_p), _c_i32, _c_p, _c_p, _c_p,
-                            _c_p], _c_i32),
+                            _c_p, _c_p], _c_i32),
     "burst_tl_sum": ([_c_i32, _c_i32, _c_i32, _c_i32, _c_i64, ctypes.POINTER(_c_p), _c_i32, _c_p,
-                      _c_p], _c_i32),
+                      _c_p, _c_p], _c_i32),
+    "burst_tl_accumulate": ([_c_i32, _c_i32, _c_i32, _c_i64, _c_p, _c_p, _c_p], _c_i32),
     "burst_read_flags": ([_c_p, ctypes.POINTER(_c_i32)], _c_i32),
-    "burst_set_bwd_variant": ([_c_i32], _c_i32),
-    "burst_set_fwd_variant": ([_c_i32], _c_i32),
     "burst_ipc_handle_bytes": ([], _c_sz),
     "burst_ipc_alloc": ([_c_sz, ctypes.POINTER(_c_p)], _c_i32),
     "burst_ipc_free": ([_c_p], _c_i32),

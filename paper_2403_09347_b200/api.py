@@ -19,7 +19,7 @@ import torch
 
 from .errors import ConfigError, ShapeError
 from .masks import GridMask
-from .kernels import CudaKernels, check_qkv, default_scale
+from .kernels import PENDING, CudaKernels, check_errors, check_qkv, default_scale
 from .ring import (IpcTransport, NcclTransport, SoloTransport, ring_backward,
                    ring_backward_qtravel, ring_forward, run_ranks)
 from .schedule import shard, unshard
@@ -56,29 +56,33 @@ def _transport_for(group, comm: str = "nccl"):
 class _BurstAttnFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, q, k, v, scale, causal, zigzag, transport, kernels, n_valid, recorders,
-                bwd_payload, grid):
+                bwd_payload, grid, check):
         rec_f, rec_b = recorders if recorders is not None else (None, None)
         o, lse = ring_forward(q, k, v, scale, causal, zigzag, transport, kernels, n_valid,
-                              recorder=rec_f, grid=grid)
+                              recorder=rec_f, grid=grid, check=check)
         ctx.save_for_backward(q, k, v, o, lse)
-        ctx.cfg = (scale, causal, zigzag, transport, kernels, n_valid, rec_b, bwd_payload, grid)
+        ctx.cfg = (scale, causal, zigzag, transport, kernels, n_valid, rec_b, bwd_payload, grid,
+                   check)
         ctx.mark_non_differentiable(lse)
+        ctx.set_materialize_grads(False)     # no zero dlse tensor per backward
         return o, lse
 
     @staticmethod
     def backward(ctx, do, _dlse):
         q, k, v, o, lse = ctx.saved_tensors
-        scale, causal, zigzag, transport, kernels, n_valid, rec_b, bwd_payload, grid = ctx.cfg
+        scale, causal, zigzag, transport, kernels, n_valid, rec_b, bwd_payload, grid, check = ctx.cfg
+        if do is None:
+            return (None,) * 13
         bwd = ring_backward_qtravel if bwd_payload == "q" else ring_backward
         dq, dk, dv = bwd(q, k, v, o, lse, do.contiguous(), scale, causal, zigzag, transport,
-                         kernels, n_valid, recorder=rec_b, grid=grid)
-        return dq, dk, dv, None, None, None, None, None, None, None, None, None
+                         kernels, n_valid, recorder=rec_b, grid=grid, check=check)
+        return dq, dk, dv, None, None, None, None, None, None, None, None, None, None
 
 
 def burst_attn_func(q, k, v, causal: bool = False, softmax_scale: float | None = None,
                     group=None, zigzag: bool | None = None, valid_len: int | None = None, *,
-                    bwd_payload: str = "kv", mask=None, comm: str = "nccl", _transport=None,
-                    _kernels=None, _recorders=None):
+                    bwd_payload: str = "kv", mask=None, comm: str = "nccl", check: str = "async",
+                    _transport=None, _kernels=None, _recorders=None):
     """BurstAttention over the ranks of `group` (NCCL ring over NVLink).
 
     q, k, v: [batch, n_local, heads, head_dim] shards of the global sequence
@@ -95,9 +99,14 @@ def burst_attn_func(q, k, v, causal: bool = False, softmax_scale: float | None =
     mask_from_spec value (dict / JSON path with n_query_blocks, n_key_blocks, skip and
     an optional causal flag; masking.py:150-180); composes with `causal`.
     `comm`: ring transport, "nccl" (default) or "ce" (copy engines + CUDA IPC, no SM).
+    `check`: when each pass's device error word (MaskError: a row with no visible key;
+    NonFiniteError: a non-finite output) is read: "async" (default) raises at a later
+    call once the pass has finished on the device, or in `check_errors()`, without
+    stalling the host; "sync" raises at the end of each pass (synchronises); "off".
     `_recorders`: optional (forward, backward) trace.PassRecorder pair that
     records this rank's measured hop timeline and byte ledger.
     """
+    PENDING.check(block=False)      # errors of earlier asynchronously checked passes
     check_qkv(q, k, v) if _kernels is None else None
     if q.shape[1] != k.shape[1]:
         raise ShapeError("ring shards must have equal query and key lengths")
@@ -110,18 +119,26 @@ def burst_attn_func(q, k, v, causal: bool = False, softmax_scale: float | None =
         zigzag = bool(causal) and transport.world > 1
     if zigzag and q.shape[1] % 2:
         raise ShapeError("zigzag shards need an even local length")
+    if zigzag and q.dtype == torch.bfloat16 and (q.shape[1] // 2) % 8:
+        # the Q_LATE_HALF hop starts at the chunk boundary; the bf16 kernels need it
+        # 8-row aligned.  Rejected here, on every rank, before any exchange is posted
+        raise ShapeError(f"bf16 zigzag shards need a chunk length (n_local / 2 = "
+                         f"{q.shape[1] // 2}) that is a multiple of 8")
+    if check not in ("sync", "async", "off"):
+        raise ConfigError(f"check must be 'sync', 'async' or 'off', got {check!r}")
     if valid_len is not None and not 0 < valid_len <= q.shape[1] * transport.world:
         raise ShapeError(f"valid_len={valid_len} outside (0, {q.shape[1] * transport.world}]")
     if bwd_payload not in ("kv", "q"):
         raise ConfigError(f"bwd_payload must be 'kv' or 'q', got {bwd_payload!r}")
-    grid, causal = _bind_mask(mask, causal, valid_len or q.shape[1] * transport.world)
+    grid, causal = _bind_mask(mask, causal, q.shape[1] * transport.world, valid_len)
     return _BurstAttnFn.apply(q, k, v, scale, bool(causal), bool(zigzag), transport, kernels,
-                              valid_len, _recorders, bwd_payload, grid)
+                              valid_len, _recorders, bwd_payload, grid, check)
 
 
-def _bind_mask(mask, causal, total):
-    """(GridMask bound to the global length or None, effective causal flag); validates
-    that every real query row keeps a visible key (BlockMask.validate, masking.py:132-147)."""
+def _bind_mask(mask, causal, total, n_valid=None):
+    """(GridMask bound to the global (padded) length or None, effective causal flag);
+    validates that every real query row keeps a visible key (BlockMask.validate,
+    masking.py:132-147)."""
     if mask is None:
         return None, causal
     if isinstance(mask, GridMask):
@@ -132,7 +149,7 @@ def _bind_mask(mask, causal, total):
     if grid is None:
         return None, causal
     grid = grid.bind(total)
-    grid.validate(causal)
+    grid.validate(causal, n_valid)
     return grid, causal
 
 
@@ -150,7 +167,7 @@ class PassResult:
 def run_ring_pass(q, k, v, world: int, causal: bool = False, softmax_scale: float | None = None,
                   dout=None, zigzag: bool | None = None, kernels=None,
                   pad: bool = False, trace: bool = False,
-                  bwd_payload: str = "kv", mask=None) -> PassResult:
+                  bwd_payload: str = "kv", mask=None, check: str = "sync") -> PassResult:
     """Whole-ring forward (+ backward when `dout` is given) of GLOBAL tensors
     [batch, N, heads, head_dim] over `world` simulated devices on this GPU.
 
@@ -187,7 +204,9 @@ def run_ring_pass(q, k, v, world: int, causal: bool = False, softmax_scale: floa
         q, k, v = padz(q), padz(k), padz(v)
         dout = padz(dout) if dout is not None else None
     scale = default_scale(q.shape[-1]) if softmax_scale is None else float(softmax_scale)
-    grid, causal = _bind_mask(mask, causal, N)   # cells tile the real length (padding excluded)
+    # the reference applies the grid over the padded length n_total (ring.py:170, 233;
+    # masking.py:48-63 cell bounds over `total`) and validates the real rows
+    grid, causal = _bind_mask(mask, causal, q.shape[1], n_valid)
     shards = [[shard(t, r, world, zigzag) for r in range(world)] for t in (q, k, v)]
     do_sh = [shard(dout, r, world, zigzag) for r in range(world)] if dout is not None else None
 
@@ -197,12 +216,12 @@ def run_ring_pass(q, k, v, world: int, causal: bool = False, softmax_scale: floa
     def one(rank, transport):
         qs, ks, vs = shards[0][rank], shards[1][rank], shards[2][rank]
         o, lse = ring_forward(qs, ks, vs, scale, causal, zigzag, transport, kernels, n_valid,
-                              recorder=rec_f[rank], grid=grid)
+                              recorder=rec_f[rank], grid=grid, check=check)
         if do_sh is None:
             return o, lse, None
         bwd = ring_backward_qtravel if bwd_payload == "q" else ring_backward
         g = bwd(qs, ks, vs, o, lse, do_sh[rank], scale, causal, zigzag, transport, kernels,
-                n_valid, recorder=rec_b[rank], grid=grid)
+                n_valid, recorder=rec_b[rank], grid=grid, check=check)
         return o, lse, g
 
     res = run_ranks(world, one)

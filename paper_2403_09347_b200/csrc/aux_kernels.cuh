@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(256) tl_rows_kernel(int H, int D, int64_t n, P
   }
   __syncthreads();
   const int64_t b = bh / H, h = bh % H;
+  float nf = 0.f;   // NaN iff an output value is non-finite (x * 0 = NaN for inf / NaN)
   for (int k = threadIdx.x; k < nc4 * 128; k += 256) {
     const int r = k / nc4, g = k % nc4;
     const int64_t row = tile * 128 + r;
@@ -146,11 +147,29 @@ __global__ void __launch_bounds__(256) tl_rows_kernel(int H, int D, int64_t n, P
       const float inv = lv > 0.f ? 1.f / lv : 0.f;
       v.x *= inv; v.y *= inv; v.z *= inv; v.w *= inv;
       if (cg == 0 && g == 0) {
-        lse[bh * n + row] = lv > 0.f ? (m[bh * n + row] + log2f(lv)) * kLn2 : -INFINITY;
-        if (!(lv > 0.f)) atomicOr(flags, 1);
+        const float ls = lv > 0.f ? (m[bh * n + row] + log2f(lv)) * kLn2 : -INFINITY;
+        lse[bh * n + row] = ls;
+        if (lv == 0.f) atomicOr(flags, 1);                // MaskError
+        else nf = fmaf(ls, 0.f, nf);
       }
     }
+    nf = fmaf(v.x, 0.f, fmaf(v.y, 0.f, fmaf(v.z, 0.f, fmaf(v.w, 0.f, nf))));
     st4<T>(out + ((b * n + row) * H + h) * D + cg * cw + g * 4, v.x, v.y, v.z, v.w);
+  }
+  // NonFiniteError (bit 1): every public output is checked once (linalg.py:253-255)
+  if (__syncthreads_or(!(fabsf(nf) <= 3.0e38f)) && threadIdx.x == 0) atomicOr(flags, 2);
+}
+
+// acc += part over a TL workspace (float4 grid-stride): folds a dK/dV (or dQ)
+// contribution into the home accumulator as soon as its exchange has landed, so a
+// rank holds O(1) contribution buffers whatever the ring size (ring.py:239-241
+// accumulates in place the same way).
+__global__ void tl_accumulate_kernel(int64_t n4, float4* __restrict__ acc,
+                                     const float4* __restrict__ part) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 a = acc[i], c = part[i];
+    acc[i] = make_float4(a.x + c.x, a.y + c.y, a.z + c.z, a.w + c.w);
   }
 }
 

@@ -9,17 +9,15 @@
 #include <cstring>
 #include <atomic>
 #include <mutex>
+#include <set>
+#include <utility>
 #include <string>
 
 #include "../../include/burst_b200.h"
 #include "aux_kernels.cuh"
-#include "lao_bwd3_sm100.cuh"
 #include "lao_bwd4_sm100.cuh"
-#include "lao_bwd5_sm100.cuh"
-#include "lao_bwd6_sm100.cuh"
 #include "lao_bwd_sm100.cuh"
 #include "lao_fwd_sm100.cuh"
-#include "lao_fwd2_sm100.cuh"
 #include "simt_f32.cuh"
 
 using namespace burst;
@@ -145,11 +143,24 @@ int check_hop(const burst_hop* h) {
   return BURST_OK;
 }
 
+// The dynamic-SMEM opt-in is a per-device (per-context) function attribute: set it
+// once for every (kernel, device) pair this process launches on.
 template <typename K>
 int set_smem(K kernel, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  const auto key = std::make_pair(reinterpret_cast<const void*>(kernel), dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count(key)) return BURST_OK;
   CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.insert(key);
   return BURST_OK;
 }
+
+int* flags_of(const burst_hop* h) { return h->flags ? h->flags : device_flags(); }
+int* flags_or_default(int32_t* f) { return f ? f : device_flags(); }
 
 int grid_for(int64_t work, int block) {
   int64_t g = (work + block - 1) / block;
@@ -167,20 +178,15 @@ int launch_fwd_bf16(const burst_hop* h, const void* q, const void* k, const void
   if ((rc = make_tmap(&p.tm_k, k, h->n_k, h->heads, D, h->batch))) return rc;
   if ((rc = make_tmap(&p.tm_v, v, h->n_k, h->heads, D, h->batch))) return rc;
   p.o_acc = o_acc; p.m_run = m; p.l_run = l; p.o_out = o_out; p.lse_out = lse;
-  p.flags = device_flags();
+  p.flags = flags_of(h);
   p.hop = *h;
   p.scale_log2 = h->softmax_scale * kLog2e;
   p.first_hop = first; p.finalize = fin;
 #ifdef BURST_TRACE
   p.trace = trace_buffer();
 #endif
-  static std::once_flag once;
-  static int attr_rc = 0;
-  std::call_once(once, [] {
-    attr_rc = set_smem(fwd::lao_fwd_kernel<D, false>, fwd::Cfg<D>::kSmemBytes);
-    if (!attr_rc) attr_rc = set_smem(fwd::lao_fwd_kernel<D, true>, fwd::Cfg<D>::kSmemBytes);
-  });
-  if (attr_rc) return attr_rc;
+  if ((rc = set_smem(fwd::lao_fwd_kernel<D, false>, fwd::Cfg<D>::kSmemBytes))) return rc;
+  if ((rc = set_smem(fwd::lao_fwd_kernel<D, true>, fwd::Cfg<D>::kSmemBytes))) return rc;
   dim3 grid((unsigned)ceil_div(h->q_len, 2 * fwd::BM), h->heads, h->batch);
   if (h->grid_skip)
     fwd::lao_fwd_kernel<D, true><<<grid, fwd::kThreads, fwd::Cfg<D>::kSmemBytes, st>>>(p);
@@ -190,49 +196,13 @@ int launch_fwd_bf16(const burst_hop* h, const void* q, const void* k, const void
   return BURST_OK;
 }
 
-// 64-key-tile forward with double-buffered scores (head_dim 128, dense hops).
-int launch_fwd2_bf16(const burst_hop* h, const void* q, const void* k, const void* v, float* o_acc,
-                     float* m, float* l, void* o_out, float* lse, int first, int fin, cudaStream_t st) {
-  fwd2::Params p;
-  memset(&p, 0, sizeof(p));
-  int rc;
-  if ((rc = make_tmap(&p.tm_q, q, h->n_q, h->heads, 128, h->batch))) return rc;
-  if ((rc = make_tmap(&p.tm_k, k, h->n_k, h->heads, 128, h->batch, 64))) return rc;
-  if ((rc = make_tmap(&p.tm_v, v, h->n_k, h->heads, 128, h->batch, 64))) return rc;
-  p.o_acc = o_acc; p.m_run = m; p.l_run = l; p.o_out = o_out; p.lse_out = lse;
-  p.flags = device_flags();
-  p.hop = *h;
-  p.scale_log2 = h->softmax_scale * kLog2e;
-  p.first_hop = first; p.finalize = fin;
-  static std::once_flag once;
-  static int attr_rc = 0;
-  std::call_once(once, [] { attr_rc = set_smem(fwd2::lao_fwd2_kernel, fwd2::kSmemBytes); });
-  if (attr_rc) return attr_rc;
-  dim3 grid((unsigned)ceil_div(h->q_len, 2 * fwd2::BM), h->heads, h->batch);
-  fwd2::lao_fwd2_kernel<<<grid, fwd2::kThreads, fwd2::kSmemBytes, st>>>(p);
-  CHECK_LAUNCH();
-  return BURST_OK;
-}
-
-// Forward kernel for bf16 head_dim 128 (BURST_FWD_KERNEL / burst_set_fwd_variant:
-// 1 = 128-key tiles (lao_fwd), 2 = 64-key tiles with double-buffered scores (lao_fwd2)).
-std::atomic<int> g_fwd_override{0};
-int fwd_variant() {
-  static int v = [] {
-    const char* e = getenv("BURST_FWD_KERNEL");
-    return (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 1;
-  }();
-  const int o = g_fwd_override.load(std::memory_order_relaxed);
-  return o ? o : v;
-}
-
 template <int D>
 int launch_fwd_f32(const burst_hop* h, const void* q, const void* k, const void* v, float* o_acc,
                    float* m, float* l, void* o_out, float* lse, int first, int fin, cudaStream_t st) {
   simt::FwdParams p;
   p.q = (const float*)q; p.k = (const float*)k; p.v = (const float*)v;
   p.o_acc = o_acc; p.m_run = m; p.l_run = l; p.o_out = (float*)o_out; p.lse_out = lse;
-  p.flags = device_flags();
+  p.flags = flags_of(h);
   p.hop = *h;
   p.scale_log2 = h->softmax_scale * kLog2e;
   p.first_hop = first; p.finalize = fin;
@@ -254,123 +224,16 @@ int launch_bwd_bf16(const burst_hop* h, const void* q, const void* k, const void
   if ((rc = make_tmap(&p.tm_v, v, h->n_k, h->heads, D, h->batch))) return rc;
   p.stats = stats; p.dq_acc = dq_acc; p.dk_acc = dk; p.dv_acc = dv;
   p.hop = *h;
+  p.hop.flags = flags_of(h);
   p.scale_log2 = h->softmax_scale * kLog2e;
   p.scale = h->softmax_scale;
   p.accumulate = acc;
 #ifdef BURST_TRACE
   p.trace = trace_buffer();
 #endif
-  static std::once_flag once;
-  static int attr_rc = 0;
-  std::call_once(once, [] { attr_rc = set_smem(bwd::lao_bwd_kernel<D>, bwd::Cfg<D>::kSmemBytes); });
-  if (attr_rc) return attr_rc;
+  if ((rc = set_smem(bwd::lao_bwd_kernel<D>, bwd::Cfg<D>::kSmemBytes))) return rc;
   dim3 grid((unsigned)ceil_div(h->k_len, bwd::BN), h->heads, h->batch);
   bwd::lao_bwd_kernel<D><<<grid, bwd::kThreads, bwd::Cfg<D>::kSmemBytes, st>>>(p);
-  CHECK_LAUNCH();
-  return BURST_OK;
-}
-
-// CTA-pair backward with two P/dS warpgroups and SMEM-staged dQ reduction (variant 5).
-int launch_bwd5_bf16(const burst_hop* h, const void* q, const void* k, const void* v, const void* dout,
-                     const float* stats, float* dq_acc, float* dk, float* dv, int acc, cudaStream_t st) {
-  bwd5::Params p;
-  memset(&p, 0, sizeof(p));
-  int rc;
-  if ((rc = make_tmap(&p.tm_q128, q, h->n_q, h->heads, 128, h->batch))) return rc;
-  if ((rc = make_tmap(&p.tm_q64, q, h->n_q, h->heads, 128, h->batch, 64))) return rc;
-  if ((rc = make_tmap(&p.tm_do128, dout, h->n_q, h->heads, 128, h->batch))) return rc;
-  if ((rc = make_tmap(&p.tm_do64, dout, h->n_q, h->heads, 128, h->batch, 64))) return rc;
-  if ((rc = make_tmap(&p.tm_k, k, h->n_k, h->heads, 128, h->batch))) return rc;
-  if ((rc = make_tmap(&p.tm_v, v, h->n_k, h->heads, 128, h->batch))) return rc;
-  if ((rc = make_tmap_tl(&p.tm_dq, dq_acc, h->n_q, h->heads, 128, h->batch))) return rc;
-  p.stats = stats; p.dq_acc = dq_acc; p.dk_acc = dk; p.dv_acc = dv;
-  p.hop = *h;
-  p.scale_log2 = h->softmax_scale * kLog2e;
-  p.scale = h->softmax_scale;
-  p.accumulate = acc;
-#ifdef BURST_TRACE
-  p.trace = trace_buffer();
-#endif
-  static std::once_flag once;
-  static int attr_rc = 0;
-  std::call_once(once, [] { attr_rc = set_smem(bwd5::lao_bwd5_kernel, bwd5::kSmemBytes); });
-  if (attr_rc) return attr_rc;
-  dim3 grid((unsigned)(2 * ceil_div(h->k_len, 2 * bwd5::BN)), h->heads, h->batch);
-  bwd5::lao_bwd5_kernel<<<grid, bwd5::kThreads, bwd5::kSmemBytes, st>>>(p);
-  CHECK_LAUNCH();
-  return BURST_OK;
-}
-
-// CTA-pair backward with the dS exchange and dQ off the critical path (variant 6).
-int launch_bwd6_bf16(const burst_hop* h, const void* q, const void* k, const void* v, const void* dout,
-                     const float* stats, float* dq_acc, float* dk, float* dv, int acc, cudaStream_t st) {
-  bwd6::Params p;
-  memset(&p, 0, sizeof(p));
-  int rc;
-  if ((rc = make_tmap(&p.tm_q128, q, h->n_q, h->heads, 128, h->batch))) return rc;
-  if ((rc = make_tmap(&p.tm_q64, q, h->n_q, h->heads, 128, h->batch, 64))) return rc;
-  if ((rc = make_tmap(&p.tm_do128, dout, h->n_q, h->heads, 128, h->batch))) return rc;
-  if ((rc = make_tmap(&p.tm_do64, dout, h->n_q, h->heads, 128, h->batch, 64))) return rc;
-  if ((rc = make_tmap(&p.tm_k, k, h->n_k, h->heads, 128, h->batch))) return rc;
-  if ((rc = make_tmap(&p.tm_v, v, h->n_k, h->heads, 128, h->batch))) return rc;
-  if ((rc = make_tmap_tl(&p.tm_dq, dq_acc, h->n_q, h->heads, 128, h->batch))) return rc;
-  p.stats = stats; p.dq_acc = dq_acc; p.dk_acc = dk; p.dv_acc = dv;
-  p.hop = *h;
-  p.scale_log2 = h->softmax_scale * kLog2e;
-  p.scale = h->softmax_scale;
-  p.accumulate = acc;
-#ifdef BURST_TRACE
-  p.trace = trace_buffer();
-#endif
-  static std::once_flag once;
-  static int attr_rc = 0;
-  std::call_once(once, [] { attr_rc = set_smem(bwd6::lao_bwd6_kernel, bwd6::kSmemBytes); });
-  if (attr_rc) return attr_rc;
-  dim3 grid((unsigned)(2 * ceil_div(h->k_len, 2 * bwd6::BN)), h->heads, h->batch);
-  bwd6::lao_bwd6_kernel<<<grid, bwd6::kThreads, bwd6::kSmemBytes, st>>>(p);
-  CHECK_LAUNCH();
-  return BURST_OK;
-}
-
-// Backward kernel variant for bf16 (BURST_BWD_KERNEL: 1 = single CTA + red.global,
-// 2 = alias of 5, 3 = single CTA + SMEM-staged TMA bulk reductions, 4 = variant 3 with two
-// P/dS warpgroups and a double-buffered dQ drain, 5 = CTA pair with two P/dS warpgroups,
-// dS^T in TMEM and SMEM-staged dQ reduction; default 4).
-std::atomic<int> g_bwd_override{0};   // burst_set_bwd_variant (0 = env / default)
-
-int bwd_variant() {
-  static int v = [] {
-    const char* e = getenv("BURST_BWD_KERNEL");
-    return (e && e[0] >= '1' && e[0] <= '6') ? e[0] - '0' : 4;
-  }();
-  const int o = g_bwd_override.load(std::memory_order_relaxed);
-  return o ? o : v;
-}
-
-template <int D>
-int launch_bwd3_bf16(const burst_hop* h, const void* q, const void* k, const void* v, const void* dout,
-                     const float* stats, float* dq_acc, float* dk, float* dv, int acc, cudaStream_t st) {
-  bwd3::Params p;
-  memset(&p, 0, sizeof(p));
-  int rc;
-  if ((rc = make_tmap(&p.tm_q, q, h->n_q, h->heads, D, h->batch))) return rc;
-  if ((rc = make_tmap(&p.tm_do, dout, h->n_q, h->heads, D, h->batch))) return rc;
-  if ((rc = make_tmap(&p.tm_k, k, h->n_k, h->heads, D, h->batch))) return rc;
-  if ((rc = make_tmap(&p.tm_v, v, h->n_k, h->heads, D, h->batch))) return rc;
-  p.stats = stats; p.dq_acc = dq_acc; p.dk_acc = dk; p.dv_acc = dv;
-  p.hop = *h;
-  p.scale_log2 = h->softmax_scale * kLog2e;
-  p.scale = h->softmax_scale;
-  p.accumulate = acc;
-#ifdef BURST_TRACE
-  p.trace = trace_buffer();
-#endif
-  static std::once_flag once;
-  static int attr_rc = 0;
-  std::call_once(once, [] { attr_rc = set_smem(bwd3::lao_bwd3_kernel<D>, bwd3::Cfg<D>::kSmemBytes); });
-  if (attr_rc) return attr_rc;
-  dim3 grid((unsigned)ceil_div(h->k_len, bwd3::BN), h->heads, h->batch);
-  bwd3::lao_bwd3_kernel<D><<<grid, bwd3::kThreads, bwd3::Cfg<D>::kSmemBytes, st>>>(p);
   CHECK_LAUNCH();
   return BURST_OK;
 }
@@ -387,19 +250,15 @@ int launch_bwd4_bf16(const burst_hop* h, const void* q, const void* k, const voi
   if ((rc = make_tmap(&p.tm_v, v, h->n_k, h->heads, D, h->batch))) return rc;
   p.stats = stats; p.dq_acc = dq_acc; p.dk_acc = dk; p.dv_acc = dv;
   p.hop = *h;
+  p.hop.flags = flags_of(h);
   p.scale_log2 = h->softmax_scale * kLog2e;
   p.scale = h->softmax_scale;
   p.accumulate = acc;
 #ifdef BURST_TRACE
   p.trace = trace_buffer();
 #endif
-  static std::once_flag once;
-  static int attr_rc = 0;
-  std::call_once(once, [] {
-    attr_rc = set_smem(bwd4::lao_bwd4_kernel<D, false>, bwd4::Cfg<D>::kSmemBytes);
-    if (!attr_rc) attr_rc = set_smem(bwd4::lao_bwd4_kernel<D, true>, bwd4::Cfg<D>::kSmemBytes);
-  });
-  if (attr_rc) return attr_rc;
+  if ((rc = set_smem(bwd4::lao_bwd4_kernel<D, false>, bwd4::Cfg<D>::kSmemBytes))) return rc;
+  if ((rc = set_smem(bwd4::lao_bwd4_kernel<D, true>, bwd4::Cfg<D>::kSmemBytes))) return rc;
   dim3 grid((unsigned)ceil_div(h->k_len, bwd4::BN), h->heads, h->batch);
   if (h->grid_skip)
     bwd4::lao_bwd4_kernel<D, true><<<grid, bwd4::kThreads, bwd4::Cfg<D>::kSmemBytes, st>>>(p);
@@ -416,14 +275,12 @@ int launch_bwd_f32(const burst_hop* h, const void* q, const void* k, const void*
   p.q = (const float*)q; p.k = (const float*)k; p.v = (const float*)v; p.dout = (const float*)dout;
   p.stats = stats; p.dq_acc = dq_acc; p.dk_acc = dk; p.dv_acc = dv;
   p.hop = *h;
+  p.hop.flags = flags_of(h);
   p.scale_log2 = h->softmax_scale * kLog2e;
   p.scale = h->softmax_scale;
   p.accumulate = acc;
   const int smem = 2 * simt::kRows * (D + 1) * 4;
-  static std::once_flag once;
-  static int attr_rc = 0;
-  std::call_once(once, [smem] { attr_rc = set_smem(simt::simt_bwd_dkv_kernel<D>, smem); });
-  if (attr_rc) return attr_rc;
+  if (int rc = set_smem(simt::simt_bwd_dkv_kernel<D>, smem)) return rc;
   if (h->q_len > 0) {
     dim3 g1((unsigned)ceil_div(h->q_len, simt::kRows), h->heads, h->batch);
     simt::simt_bwd_dq_kernel<D><<<g1, simt::kRows, 0, st>>>(p);
@@ -478,11 +335,8 @@ int burst_lao_fwd(const burst_hop* hop, const void* q, const void* k, const void
   if (hop->q_len == 0) return BURST_OK;
   cudaStream_t st = (cudaStream_t)stream;
   if (hop->dtype == BURST_DTYPE_BF16) {
-    if (hop->head_dim == 128) {
-      if (fwd_variant() == 2 && !hop->grid_skip)
-        return launch_fwd2_bf16(hop, q, k, v, o_acc, m, l, o_out, lse_out, first_hop, finalize, st);
+    if (hop->head_dim == 128)
       return launch_fwd_bf16<128>(hop, q, k, v, o_acc, m, l, o_out, lse_out, first_hop, finalize, st);
-    }
     return launch_fwd_bf16<64>(hop, q, k, v, o_acc, m, l, o_out, lse_out, first_hop, finalize, st);
   }
   switch (hop->head_dim) {
@@ -496,35 +350,36 @@ int burst_lao_fwd(const burst_hop* hop, const void* q, const void* k, const void
 // (b*h, 128-row tile, 32-column group).
 static void launch_tl_rows(int dtype, bool final_, int batch, int heads, int head_dim, int64_t n,
                            const aux::Parts& parts, int nparts, void* out, const float* m,
-                           const float* l, float* lse, cudaStream_t st) {
+                           const float* l, float* lse, int* flags, cudaStream_t st) {
   const int cw = head_dim < 32 ? head_dim : 32;
   const int64_t blocks = (int64_t)batch * heads * ceil_div(n, 128) * (head_dim / cw);
   if (dtype == BURST_DTYPE_BF16) {
     if (final_)
       aux::tl_rows_kernel<__nv_bfloat16, true><<<(unsigned)blocks, 256, 0, st>>>(
-          heads, head_dim, n, parts, nparts, (__nv_bfloat16*)out, m, l, lse, device_flags());
+          heads, head_dim, n, parts, nparts, (__nv_bfloat16*)out, m, l, lse, flags);
     else
       aux::tl_rows_kernel<__nv_bfloat16, false><<<(unsigned)blocks, 256, 0, st>>>(
-          heads, head_dim, n, parts, nparts, (__nv_bfloat16*)out, m, l, lse, device_flags());
+          heads, head_dim, n, parts, nparts, (__nv_bfloat16*)out, m, l, lse, flags);
   } else {
     if (final_)
       aux::tl_rows_kernel<float, true><<<(unsigned)blocks, 256, 0, st>>>(
-          heads, head_dim, n, parts, nparts, (float*)out, m, l, lse, device_flags());
+          heads, head_dim, n, parts, nparts, (float*)out, m, l, lse, flags);
     else
       aux::tl_rows_kernel<float, false><<<(unsigned)blocks, 256, 0, st>>>(
-          heads, head_dim, n, parts, nparts, (float*)out, m, l, lse, device_flags());
+          heads, head_dim, n, parts, nparts, (float*)out, m, l, lse, flags);
   }
 }
 
 int burst_fwd_finalize(int dtype, int batch, int heads, int head_dim, int64_t n, const float* o_acc,
-                       const float* m, const float* l, void* o_out, float* lse_out, void* stream) {
+                       const float* m, const float* l, void* o_out, float* lse_out, int32_t* flags,
+                       void* stream) {
   int rc = check_dims(dtype, batch, heads, head_dim, n);
   if (rc) return rc;
   if (n == 0) return BURST_OK;
   aux::Parts pp{};
   pp.p[0] = o_acc;
   launch_tl_rows(dtype, true, batch, heads, head_dim, n, pp, 1, o_out, m, l, lse_out,
-                 (cudaStream_t)stream);
+                 flags_or_default(flags), (cudaStream_t)stream);
   CHECK_LAUNCH();
   return BURST_OK;
 }
@@ -570,19 +425,14 @@ int burst_lao_bwd(const burst_hop* hop, const void* q, const void* k, const void
   }
   if (hop->k_len == 0) return BURST_OK;
   if (hop->dtype == BURST_DTYPE_BF16) {
-    // the staged kernel reduces whole 128-row TL tiles: needs 128-aligned query ranges
-    const int var = (bwd_variant() >= 3 && hop->q_begin % 128 != 0) ? 1 : bwd_variant();
-    if (hop->head_dim == 128) {
-      if (var == 3) return launch_bwd3_bf16<128>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
-      if (var == 4) return launch_bwd4_bf16<128>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
-      if (var == 2 || var == 5)   // 2: the first pair kernel, superseded by bwd5
-        return launch_bwd5_bf16(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
-      if (var == 6) return launch_bwd6_bf16(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
-      return launch_bwd_bf16<128>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
-    }
-    if (var == 3) return launch_bwd3_bf16<64>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
-    if (var >= 4) return launch_bwd4_bf16<64>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
-    return launch_bwd_bf16<64>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
+    // lao_bwd4 reduces whole 128-row dQ tiles: query ranges that do not start on a
+    // tile (unaligned zigzag chunks) take lao_bwd, which reduces row by row
+    const bool staged = hop->q_begin % 128 == 0;
+    if (hop->head_dim == 128)
+      return staged ? launch_bwd4_bf16<128>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st)
+                    : launch_bwd_bf16<128>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
+    return staged ? launch_bwd4_bf16<64>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st)
+                  : launch_bwd_bf16<64>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
   }
   switch (hop->head_dim) {
     case 16: return launch_bwd_f32<16>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
@@ -593,10 +443,11 @@ int burst_lao_bwd(const burst_hop* hop, const void* q, const void* k, const void
 
 int burst_bwd_finalize(int dtype, int batch, int heads, int head_dim, int64_t n, const float* dq_acc,
                        const float* const* dk_parts, const float* const* dv_parts, int nparts, void* dq,
-                       void* dk, void* dv, void* stream) {
+                       void* dk, void* dv, int32_t* flags, void* stream) {
   int rc = check_dims(dtype, batch, heads, head_dim, n);
   if (rc) return rc;
   if (nparts < 0 || nparts > 16) return fail(BURST_E_SHAPE, "nparts must be in [0, 16]");
+  int* fl = flags_or_default(flags);
   if (n == 0) return BURST_OK;
   aux::Parts pk, pv;
   for (int i = 0; i < 16; ++i) {
@@ -607,18 +458,18 @@ int burst_bwd_finalize(int dtype, int batch, int heads, int head_dim, int64_t n,
   if (dq_acc) {
     aux::Parts pq{};
     pq.p[0] = dq_acc;
-    launch_tl_rows(dtype, false, batch, heads, head_dim, n, pq, 1, dq, nullptr, nullptr, nullptr, st);
+    launch_tl_rows(dtype, false, batch, heads, head_dim, n, pq, 1, dq, nullptr, nullptr, nullptr, fl, st);
   }
   if (nparts > 0) {
-    launch_tl_rows(dtype, false, batch, heads, head_dim, n, pk, nparts, dk, nullptr, nullptr, nullptr, st);
-    launch_tl_rows(dtype, false, batch, heads, head_dim, n, pv, nparts, dv, nullptr, nullptr, nullptr, st);
+    launch_tl_rows(dtype, false, batch, heads, head_dim, n, pk, nparts, dk, nullptr, nullptr, nullptr, fl, st);
+    launch_tl_rows(dtype, false, batch, heads, head_dim, n, pv, nparts, dv, nullptr, nullptr, nullptr, fl, st);
   }
   CHECK_LAUNCH();
   return BURST_OK;
 }
 
 int burst_tl_sum(int dtype, int batch, int heads, int head_dim, int64_t n, const float* const* parts,
-                 int nparts, void* out, void* stream) {
+                 int nparts, void* out, int32_t* flags, void* stream) {
   int rc = check_dims(dtype, batch, heads, head_dim, n);
   if (rc) return rc;
   if (nparts < 1 || nparts > 16) return fail(BURST_E_SHAPE, "nparts must be in [1, 16]");
@@ -627,20 +478,24 @@ int burst_tl_sum(int dtype, int batch, int heads, int head_dim, int64_t n, const
   aux::Parts pp;
   for (int i = 0; i < 16; ++i) pp.p[i] = i < nparts ? parts[i] : nullptr;
   launch_tl_rows(dtype, false, batch, heads, head_dim, n, pp, nparts, out, nullptr, nullptr, nullptr,
-                 (cudaStream_t)stream);
+                 flags_or_default(flags), (cudaStream_t)stream);
   CHECK_LAUNCH();
   return BURST_OK;
 }
 
-int burst_set_bwd_variant(int variant) {
-  if (variant < 0 || variant > 6) return fail(BURST_E_SHAPE, "backward variant must be 0 (default) .. 6");
-  g_bwd_override.store(variant, std::memory_order_relaxed);
-  return BURST_OK;
-}
-
-int burst_set_fwd_variant(int variant) {
-  if (variant < 0 || variant > 2) return fail(BURST_E_SHAPE, "forward variant must be 0 (default), 1 or 2");
-  g_fwd_override.store(variant, std::memory_order_relaxed);
+int burst_tl_accumulate(int batch, int heads, int head_dim, int64_t n, float* acc, const float* part,
+                        void* stream) {
+  if (batch < 1 || heads < 1 || n < 0) return fail(BURST_E_SHAPE, "batch/heads must be positive, n >= 0");
+  if (head_dim != 16 && head_dim != 32 && head_dim != 64 && head_dim != 128)
+    return fail(BURST_E_UNSUPPORTED, "head_dim must be 16, 32, 64 or 128");
+  if (!acc || !part) return fail(BURST_E_SHAPE, "acc and part must not be NULL");
+  if ((reinterpret_cast<uintptr_t>(acc) | reinterpret_cast<uintptr_t>(part)) & 15)
+    return fail(BURST_E_SHAPE, "TL workspaces must be 16-byte aligned");
+  const int64_t n4 = (int64_t)burst_workspace_floats(batch, heads, head_dim, n) / 4;
+  if (n4 == 0) return BURST_OK;
+  aux::tl_accumulate_kernel<<<grid_for(n4, 256), 256, 0, (cudaStream_t)stream>>>(
+      n4, reinterpret_cast<float4*>(acc), reinterpret_cast<const float4*>(part));
+  CHECK_LAUNCH();
   return BURST_OK;
 }
 

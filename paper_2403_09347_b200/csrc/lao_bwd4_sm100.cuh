@@ -92,12 +92,18 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 template <int D, bool kGrid>
 __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_constant__ Params p) {
   using C = Cfg<D>;
-  extern __shared__ uint8_t smem_raw[];
+  // SW128 tiles need 1024-byte alignment; the declaration asks the compiler for it and
+  // the runtime check below can then only fail on a toolchain that ignores it, in
+  // which case the launch reports a CudaError (flag bit 2) instead of trapping.
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem;
   {
     const uint32_t s = ptx::smem_u32(smem_raw);
     const uint32_t pad = (1024u - (s & 1023u)) & 1023u;
-    if (pad > (uint32_t)C::kMaxPad) __trap();
+    if (pad > (uint32_t)C::kMaxPad) {
+      if (threadIdx.x == 0 && p.hop.flags) atomicOr(p.hop.flags, 4);
+      return;
+    }
     smem = smem_raw + pad;
   }
   uint8_t* sK = smem;

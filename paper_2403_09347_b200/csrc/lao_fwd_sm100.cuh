@@ -440,7 +440,11 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
     const float a_hop = (m_run == -INFINITY) ? 0.f : ptx::ex2(m_run - m_new);
     const float l_new = a_old * l_old + a_hop * l_run;
     const float inv_l = (l_new > 0.f) ? 1.f / l_new : 0.f;
-    if (valid && p.finalize && !(l_new > 0.f)) atomicOr(p.flags, 1);
+    // MaskError (bit 0): a row with no visible key; NonFiniteError (bit 1): a non-finite
+    // O or lse (PartialAttn.finalize, local_attn.py:127-135).  `nf` turns NaN iff any
+    // output value is non-finite (x * 0 = NaN for x = +-inf or NaN).
+    float nf = 0.f;
+    if (valid && p.finalize && l_new == 0.f) atomicOr(p.flags, 1);
 #pragma unroll
     for (int cc = 0; cc < D / 32; ++cc) {
       uint32_t r[32];
@@ -471,6 +475,8 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
 #pragma unroll
         for (int i = 0; i < 32; i += 8) {
           uint4 w;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) nf = fmaf(o[i + e] * inv_l, 0.f, nf);
           w.x = ptx::pack_bf16(o[i + 0] * inv_l, o[i + 1] * inv_l);
           w.y = ptx::pack_bf16(o[i + 2] * inv_l, o[i + 3] * inv_l);
           w.z = ptx::pack_bf16(o[i + 4] * inv_l, o[i + 5] * inv_l);
@@ -481,7 +487,9 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
     }
     if (valid) {
       if (p.finalize) {
-        p.lse_out[bh * hp.n_q + row] = (l_new > 0.f) ? (m_new + __log2f(l_new)) * kLn2 : -INFINITY;
+        const float lse = (l_new > 0.f) ? (m_new + __log2f(l_new)) * kLn2 : -INFINITY;
+        p.lse_out[bh * hp.n_q + row] = lse;
+        if (l_new != 0.f && !(fabsf(nf + lse) <= 3.0e38f)) atomicOr(p.flags, 2);
       } else {
         p.m_run[bh * hp.n_q + row] = m_new;
         p.l_run[bh * hp.n_q + row] = l_new;

@@ -110,20 +110,25 @@ __global__ void __launch_bounds__(kRows) simt_fwd_kernel(const FwdParams p) {
   const float a_old = (m_old == -INFINITY) ? 0.f : exp2f(m_old - mn);
   const float a_hop = (m == -INFINITY) ? 0.f : exp2f(m - mn);
   const float ln = a_old * l_old + a_hop * l;
-  if (p.finalize && !(ln > 0.f)) atomicOr(p.flags, 1);
+  if (p.finalize && ln == 0.f) atomicOr(p.flags, 1);   // MaskError
+  float nf = 0.f;                                      // NaN iff an output is non-finite
   const float inv = ln > 0.f ? 1.f / ln : 0.f;
 #pragma unroll
   for (int c = 0; c < D; ++c) {
     const size_t ti = tl_index(bh, row, c, D, NT);
     const float prev = p.first_hop ? 0.f : p.o_acc[ti];
     const float val = a_old * prev + a_hop * o[c];
-    if (p.finalize)
+    if (p.finalize) {
       p.o_out[(((int64_t)b * hp.n_q + row) * hp.heads + h) * D + c] = val * inv;
+      nf = fmaf(val * inv, 0.f, nf);
+    }
     else
       p.o_acc[ti] = val;
   }
   if (p.finalize) {
-    p.lse_out[bh * hp.n_q + row] = ln > 0.f ? (mn + log2f(ln)) * kLn2 : -INFINITY;
+    const float lse = ln > 0.f ? (mn + log2f(ln)) * kLn2 : -INFINITY;
+    p.lse_out[bh * hp.n_q + row] = lse;
+    if (ln != 0.f && !(fabsf(nf + lse) <= 3.0e38f)) atomicOr(p.flags, 2);   // NonFiniteError
   } else {
     p.m_run[bh * hp.n_q + row] = mn;
     p.l_run[bh * hp.n_q + row] = ln;

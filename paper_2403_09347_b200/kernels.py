@@ -17,12 +17,13 @@ from __future__ import annotations
 
 import ctypes
 import math
+import threading
 from dataclasses import dataclass
 
 import torch
 
 from . import _lib
-from .errors import CudaError, ShapeError
+from .errors import CudaError, MaskError, NonFiniteError, ShapeError
 from .schedule import HopPlan
 
 _DTYPES = {torch.bfloat16: _lib.DTYPE_BF16, torch.float32: _lib.DTYPE_F32}
@@ -72,19 +73,84 @@ def ws_floats(B: int, H: int, D: int, n: int) -> int:
 
 @dataclass
 class FwdState:
-    """Running (O_acc, m, l) of the pinned query block (PartialAttn, local_attn.py:66-99)."""
-    o_acc: torch.Tensor   # TL fp32 workspace
-    m: torch.Tensor       # [B, H, n] fp32, log2 units
-    l: torch.Tensor       # [B, H, n] fp32
+    """Running (O_acc, m, l) of the pinned query block (PartialAttn, local_attn.py:66-99),
+    None for a one-hop pass, and the pass's device error word."""
+    o_acc: torch.Tensor | None   # TL fp32 workspace
+    m: torch.Tensor | None       # [B, H, n] fp32, log2 units
+    l: torch.Tensor | None       # [B, H, n] fp32
+    flags: torch.Tensor          # [1] int32 (burst_hop.flags)
 
 
 @dataclass
 class BwdState:
     stats: torch.Tensor   # [2, B*H, ceil(n/128)*128]: lse*log2e, D
     dq_acc: torch.Tensor  # TL fp32
+    flags: torch.Tensor   # [1] int32 error word of the pass
 
 
-def make_hop(plan: HopPlan, q: torch.Tensor, k: torch.Tensor, scale: float) -> _lib.Hop:
+# bits of the device error word (include/burst_b200.h burst_hop.flags)
+FLAG_MASK, FLAG_NONFINITE, FLAG_LAUNCH = 1, 2, 4
+
+
+def raise_for_flags(bits: int, where: str) -> None:
+    """Map the device error word onto the reference taxonomy: MaskError first (a row
+    with no visible key), then NonFiniteError (PartialAttn.finalize order,
+    local_attn.py:127-135; linalg._ensure_finite, linalg.py:253-255)."""
+    if bits & FLAG_MASK:
+        raise MaskError(f"{where}: some query row accumulated no unmasked entries")
+    if bits & FLAG_NONFINITE:
+        raise NonFiniteError(f"{where} produced a non-finite value")
+    if bits & FLAG_LAUNCH:
+        raise CudaError(f"{where}: a kernel could not run (shared-memory alignment)")
+
+
+class _Pending:
+    """Error words copied to pinned host memory at the end of passes run with
+    check="async"; raised at the next pass entry once the copy has landed, or by
+    check_errors() (blocking)."""
+
+    def __init__(self):
+        self.lock = threading.Lock()
+        self.items = []      # (host int32 tensor, event, where)
+
+    def add(self, flags: torch.Tensor, stream, where: str) -> None:
+        host = torch.empty(1, dtype=torch.int32, pin_memory=True)
+        with torch.cuda.stream(stream) if stream is not None else _nullctx():
+            host.copy_(flags, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+        with self.lock:
+            self.items.append((host, ev, where))
+
+    def check(self, block: bool) -> None:
+        with self.lock:
+            items, keep = self.items, []
+            self.items = []
+            bad = None
+            for host, ev, where in items:
+                if block:
+                    ev.synchronize()
+                elif not ev.query():
+                    keep.append((host, ev, where))
+                    continue
+                if bad is None and int(host[0]) != 0:
+                    bad = (int(host[0]), where)
+            self.items = keep
+        if bad is not None:
+            raise_for_flags(*bad)
+
+
+PENDING = _Pending()
+
+
+def check_errors() -> None:
+    """Raise the first error recorded by an asynchronously checked pass (blocks until
+    every such pass has finished on the device)."""
+    PENDING.check(block=True)
+
+
+def make_hop(plan: HopPlan, q: torch.Tensor, k: torch.Tensor, scale: float,
+             flags: torch.Tensor | None = None) -> _lib.Hop:
     B, n_q, H, D = q.shape
     h = _lib.Hop()
     h.batch, h.heads, h.head_dim, h.dtype = B, H, D, dtype_code(q)
@@ -100,6 +166,8 @@ def make_hop(plan: HopPlan, q: torch.Tensor, k: torch.Tensor, scale: float) -> _
         h.grid_skip = g.device_table(q.device).data_ptr()
         h.grid_nqb, h.grid_nkb = g.n_query_blocks, g.n_key_blocks
         h.grid_qcell, h.grid_kcell = g.qcell, g.kcell
+    if flags is not None:
+        h.flags = flags.data_ptr()
     return h
 
 
@@ -112,12 +180,20 @@ class CudaKernels:
         _lib.load()
 
     # ------------------------------------------------------------ allocation
-    def fwd_state(self, q: torch.Tensor) -> FwdState:
+    @staticmethod
+    def _flags(device) -> torch.Tensor:
+        return torch.zeros(1, dtype=torch.int32, device=device)
+
+    def fwd_state(self, q: torch.Tensor, running: bool = True) -> FwdState:
+        """Running state of a pass (none needed when one hop finalizes directly)."""
         B, n, H, D = q.shape
         dev = q.device
+        if not running:
+            return FwdState(None, None, None, self._flags(dev))
         return FwdState(torch.empty(ws_floats(B, H, D, n), dtype=torch.float32, device=dev),
                         torch.empty(B, H, n, dtype=torch.float32, device=dev),
-                        torch.empty(B, H, n, dtype=torch.float32, device=dev))
+                        torch.empty(B, H, n, dtype=torch.float32, device=dev),
+                        self._flags(dev))
 
     def part(self, k: torch.Tensor) -> torch.Tensor:
         """One fp32 dK or dV contribution buffer for a visiting block (TL layout)."""
@@ -127,34 +203,61 @@ class CudaKernels:
     # ------------------------------------------------------------ forward
     def fwd(self, plan: HopPlan, q, k, v, scale: float, state: FwdState | None, o, lse,
             first: bool, finalize: bool, stream=None) -> None:
-        hop = make_hop(plan, q, k, scale)
+        """One hop; `state` None: a single finalizing hop on the per-device error word."""
+        st = state if state is not None else FwdState(None, None, None, None)
+        hop = make_hop(plan, q, k, scale, st.flags)
         _lib.call("burst_lao_fwd", ctypes.byref(hop), _ptr(q), _ptr(k), _ptr(v),
-                  _ptr(state.o_acc if state else None), _ptr(state.m if state else None),
-                  _ptr(state.l if state else None), _ptr(o if finalize else None),
+                  _ptr(st.o_acc), _ptr(st.m), _ptr(st.l), _ptr(o if finalize else None),
                   _ptr(lse if finalize else None), int(first), int(finalize),
                   _stream_handle(stream))
 
     def fwd_finalize(self, state: FwdState, o, lse, stream=None) -> None:
         B, n, H, D = o.shape
         _lib.call("burst_fwd_finalize", dtype_code(o), B, H, D, n, _ptr(state.o_acc),
-                  _ptr(state.m), _ptr(state.l), _ptr(o), _ptr(lse), _stream_handle(stream))
+                  _ptr(state.m), _ptr(state.l), _ptr(o), _ptr(lse), _ptr(state.flags),
+                  _stream_handle(stream))
+
+    # ------------------------------------------------------------ error boundary
+    def finish(self, state, check: str, stream=None, where: str = "BurstAttention") -> None:
+        """Read the pass's device error word once: "sync" raises here (synchronises
+        the stream), "async" copies it to pinned memory and raises at a later pass
+        entry or in check_errors(), "off" skips the check."""
+        if check == "off":
+            return
+        if check == "sync":
+            s = stream if stream is not None else torch.cuda.current_stream()
+            s.synchronize()
+            raise_for_flags(int(state.flags.item()), where)
+        elif check == "async":
+            PENDING.add(state.flags, stream, where)
+        else:
+            raise ValueError(f"check must be 'sync', 'async' or 'off', got {check!r}")
 
     # ------------------------------------------------------------ backward
     def bwd_prepare(self, o, dout, lse, stream=None) -> BwdState:
         B, n, H, D = o.shape
         nt = -(-n // 128) * 128
+        with torch.cuda.stream(stream) if stream is not None else _nullctx():
+            flags = self._flags(o.device)
         st = BwdState(torch.empty(2, B * H, nt, dtype=torch.float32, device=o.device),
-                      torch.empty(ws_floats(B, H, D, n), dtype=torch.float32, device=o.device))
+                      torch.empty(ws_floats(B, H, D, n), dtype=torch.float32, device=o.device),
+                      flags)
         _lib.call("burst_bwd_preprocess", dtype_code(o), B, H, D, n, _ptr(o), _ptr(dout),
                   _ptr(lse), _ptr(st.stats), _ptr(st.dq_acc), _stream_handle(stream))
         return st
 
     def bwd(self, plan: HopPlan, q, k, v, dout, scale: float, st: BwdState, dk_part, dv_part,
             accumulate: bool, stream=None) -> None:
-        hop = make_hop(plan, q, k, scale)
+        hop = make_hop(plan, q, k, scale, st.flags)
         _lib.call("burst_lao_bwd", ctypes.byref(hop), _ptr(q), _ptr(k), _ptr(v), _ptr(dout),
                   _ptr(st.stats), _ptr(st.dq_acc), _ptr(dk_part), _ptr(dv_part), int(accumulate),
                   _stream_handle(stream))
+
+    def accumulate(self, acc_pair, part_pair, like: torch.Tensor, stream=None) -> None:
+        """acc += part for a (dK, dV) pair of TL contribution buffers."""
+        B, n, H, D = like.shape
+        for a, p in zip(acc_pair, part_pair):
+            _lib.call("burst_tl_accumulate", B, H, D, n, _ptr(a), _ptr(p), _stream_handle(stream))
 
     def bwd_finalize(self, st: BwdState, dk_parts, dv_parts, dq, dk, dv, stream=None) -> None:
         B, n, H, D = dq.shape
@@ -162,7 +265,7 @@ class CudaKernels:
         arr_k = (ctypes.c_void_p * max(np_, 1))(*[p.data_ptr() for p in dk_parts])
         arr_v = (ctypes.c_void_p * max(np_, 1))(*[p.data_ptr() for p in dv_parts])
         _lib.call("burst_bwd_finalize", dtype_code(dq), B, H, D, n, _ptr(st.dq_acc), arr_k, arr_v,
-                  np_, _ptr(dq), _ptr(dk), _ptr(dv), _stream_handle(stream))
+                  np_, _ptr(dq), _ptr(dk), _ptr(dv), _ptr(st.flags), _stream_handle(stream))
 
     # ------------------------------------------------ travelling-query backward (f2)
     def stats_tensors(self, st: BwdState) -> list:
@@ -172,28 +275,42 @@ class CudaKernels:
     def visiting_state(self, st: BwdState, stats: list, dq_part) -> BwdState:
         """Backward state of a visiting query block: its statistics, and the fresh
         dQ contribution buffer this hop reduces into."""
-        return BwdState(stats[0], dq_part)
+        return BwdState(stats[0], dq_part, st.flags)
 
-    def dq_part(self, q: torch.Tensor, stream=None) -> torch.Tensor:
-        """A zeroed fp32 dQ contribution buffer (TL layout) for a visiting block."""
+    def dq_part(self, q: torch.Tensor, stream=None, reuse: torch.Tensor | None = None) -> torch.Tensor:
+        """A zeroed fp32 dQ contribution buffer (TL layout) for a visiting block,
+        zeroed on `stream` (`reuse`: an earlier buffer to zero again)."""
         B, n, H, D = q.shape
-        buf = torch.empty(ws_floats(B, H, D, n), dtype=torch.float32, device=q.device)
+        buf = reuse if reuse is not None else torch.empty(ws_floats(B, H, D, n),
+                                                          dtype=torch.float32, device=q.device)
         with torch.cuda.stream(stream) if stream is not None else _nullctx():
             buf.zero_()
         return buf
 
-    def tl_sum(self, parts, out, stream=None) -> None:
+    def dq_recv(self, q: torch.Tensor) -> torch.Tensor:
+        """Receive buffer for a dQ contribution (fully overwritten by the exchange)."""
+        B, n, H, D = q.shape
+        return torch.empty(ws_floats(B, H, D, n), dtype=torch.float32, device=q.device)
+
+    def accumulate_dq(self, st: BwdState, part: torch.Tensor, like: torch.Tensor,
+                      stream=None) -> None:
+        """Fold a received dQ contribution into the home dQ accumulator."""
+        B, n, H, D = like.shape
+        _lib.call("burst_tl_accumulate", B, H, D, n, _ptr(st.dq_acc), _ptr(part),
+                  _stream_handle(stream))
+
+    def tl_sum(self, parts, out, flags=None, stream=None) -> None:
         B, n, H, D = out.shape
         arr = (ctypes.c_void_p * len(parts))(*[p.data_ptr() for p in parts])
         _lib.call("burst_tl_sum", dtype_code(out), B, H, D, n, arr, len(parts), _ptr(out),
-                  _stream_handle(stream))
+                  _ptr(flags), _stream_handle(stream))
 
     def bwd_finalize_qtravel(self, st: BwdState, dq_parts, dk_acc, dv_acc, dq, dk, dv,
                              stream=None) -> None:
         """dq = own accumulator + received contributions; dk/dv = pinned accumulators."""
-        self.tl_sum([st.dq_acc] + list(dq_parts), dq, stream)
-        self.tl_sum([dk_acc], dk, stream)
-        self.tl_sum([dv_acc], dv, stream)
+        self.tl_sum([st.dq_acc] + list(dq_parts), dq, st.flags, stream)
+        self.tl_sum([dk_acc], dk, st.flags, stream)
+        self.tl_sum([dv_acc], dv, st.flags, stream)
 
     def zero_(self, bufs, stream=None) -> None:
         """Zero contribution buffers on `stream` (a fully masked own block)."""
@@ -201,10 +318,6 @@ class CudaKernels:
             for b in bufs:
                 b.zero_()
 
-    def read_flags(self, stream=None) -> int:
-        out = ctypes.c_int32(0)
-        _lib.call("burst_read_flags", _stream_handle(stream), ctypes.byref(out))
-        return out.value
 
 
 def default_scale(head_dim: int) -> float:

@@ -100,7 +100,7 @@ class GridMask:
         n = self.total
         rows = n if real_rows is None else real_rows
         t = self.table()
-        kc = np.arange(n) // self.kcell
+        kc = np.arange(rows) // self.kcell        # padded keys are masked off (with_padding)
         for qb in range(self.n_query_blocks):
             r0, r1 = qb * self.qcell, min((qb + 1) * self.qcell, rows)
             if r0 >= r1:

@@ -396,17 +396,19 @@ class LoopbackTransport:
 # ---------------------------------------------------------------------------
 
 def ring_forward(q, k, v, scale: float, causal: bool, zigzag: bool, transport, kernels,
-                 n_valid: int | None = None, recorder=None, grid=None):
+                 n_valid: int | None = None, recorder=None, grid=None, check: str = "sync"):
     """One rank's forward pass.  Returns (O [B,n,H,D], lse [B,H,n] natural log).
     `n_valid`: real global length when the shards are zero-padded (reference pad=True).
     `recorder`: optional trace.PassRecorder (measured timeline + ledger, sim.py:118-261).
-    `grid`: optional masks.GridMask bound to the global length (BlockGrid)."""
+    `grid`: optional masks.GridMask bound to the global length (BlockGrid).
+    `check`: when the pass's device error word is read ("sync" | "async" | "off",
+    kernels.finish; MaskError / NonFiniteError as in PartialAttn.finalize)."""
     B, n, H, D = q.shape
     G, r = transport.world, transport.rank
     S = _Streams(q.device)
     o = torch.empty_like(q)
     lse = torch.empty(B, H, n, dtype=torch.float32, device=q.device)
-    state = kernels.fwd_state(q) if G > 1 else None
+    state = kernels.fwd_state(q, running=G > 1)
     cur_k, cur_v = k, v
     spare = None
     finalized = False
@@ -451,27 +453,53 @@ def ring_forward(q, k, v, scale: float, causal: bool, zigzag: bool, transport, k
                 spare = None   # never receive into the caller's tensors
     if not finalized:
         kernels.fwd_finalize(state, o, lse, stream=S.compute)
+    kernels.finish(state, check, stream=S.compute)
     return o, lse
 
 
+def split_own_hop(plan, n: int, world: int):
+    """(first, last) query-row halves of the own-block hop: `first` runs at hop 0 and
+    `last` after hop G-1, where it overlaps the final homecoming exchange (the
+    contribution of hop G-1 going home), which otherwise has no kernel to hide
+    behind (the one-hop lag of sim.py:19-21).  The later half holds the larger
+    share of a causal block (its queries see every earlier key), and the split row
+    is a multiple of 128 so both halves keep the tile-aligned backward kernel.
+    Returns (plan, None) when there is nothing to overlap (G == 1) or no aligned split."""
+    if world == 1 or plan.skip or plan.q_begin != 0 or plan.q_len != n:
+        return plan, None
+    cut = (n // 2) // 128 * 128
+    if cut == 0:
+        return plan, None
+    from dataclasses import replace
+    return replace(plan, q_len=cut), replace(plan, q_begin=cut, q_len=n - cut)
+
+
 def _part_exchange(r: int, G: int, n: int, causal: bool, zigzag: bool, hop: int, send_bufs,
-                   kernels, like_k, like_v, n_valid=None, grid=None):
-    """Ops moving the dK/dV contribution computed at `hop` to its home rank."""
-    ops, recv_bufs = [], None
+                   recv_bufs, n_valid=None, grid=None):
+    """Ops moving the dK/dV contribution computed at `hop` to its home rank, and
+    receiving into `recv_bufs` the one computed for ours.  Returns (ops, received?)."""
+    ops = []
     mine = plan_hop(r, G, hop, n, causal, zigzag, n_valid, grid)
     if not mine.skip:
         ops += [(SEND, send_bufs[0], mine.src), (SEND, send_bufs[1], mine.src)]
     c = contributor_to(r, G, hop)
     theirs = plan_hop(c, G, hop, n, causal, zigzag, n_valid, grid)
     if not theirs.skip:
-        recv_bufs = (kernels.part(like_k), kernels.part(like_v))
         ops += [(RECV, recv_bufs[0], c), (RECV, recv_bufs[1], c)]
-    return ops, recv_bufs
+    return ops, not theirs.skip
 
 
 def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: bool, transport,
-                  kernels, n_valid: int | None = None, recorder=None, grid=None):
+                  kernels, n_valid: int | None = None, recorder=None, grid=None,
+                  check: str = "sync"):
     """One rank's backward pass.  Returns (dq, dk, dv) in q's dtype.
+
+    Contribution buffers are O(1) in the ring size: `own` accumulates this rank's
+    dK/dV, `send[2]` hold the contributions of the last two hops (each goes home one
+    hop later), `recv` the contribution arriving for our block, folded into `own`
+    (burst_tl_accumulate) before the next hop -- the in-place accumulation of
+    ring.backward_step (ring.py:239-241).  The own block is computed in two query
+    halves (split_own_hop) so the final homecoming exchange overlaps a kernel.
     `recorder`: optional trace.PassRecorder (see ring_forward)."""
     B, n, H, D = q.shape
     G, r = transport.world, transport.rank
@@ -480,16 +508,23 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     own = (kernels.part(k), kernels.part(v))
     send = [None, None]
-    received = []
+    recv = (kernels.part(k), kernels.part(v)) if G > 1 else None
+    pending = False              # `recv` holds a contribution not yet folded into `own`
+    own_last = None              # second query half of the own block (after hop G-1)
     cur_k, cur_v = k, v
     spare = None
-    prev = S.compute_mark()
     for h in range(G):
         plan = plan_hop(r, G, h, n, causal, zigzag, n_valid, grid)
-        # the hop's kernel first, then the transfers (which wait only for hop h-1's
-        # kernel: it produced the contribution sent now and last read `spare`)
+        if h == 0:
+            plan, own_last = split_own_hop(plan, n, G)
         if recorder is not None:
             recorder.mark(h, "compute_start", S.compute)
+        if pending:              # landed in the previous slot (compute waited for it)
+            kernels.accumulate(own, recv, k, stream=S.compute)
+            pending = False
+        # this slot's transfers wait for everything above: hop h-1's kernel (it made
+        # the contribution sent now and last read `spare`) and the fold of `recv`
+        ready = S.compute_mark()
         if h == 0:
             target = own
         else:
@@ -503,7 +538,6 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
             kernels.zero_(target, stream=S.compute)
         if recorder is not None:
             recorder.mark(h, "compute_end", S.compute)
-        done = S.compute_mark()
         ops = []
         if h < G - 1:
             if spare is None:
@@ -512,16 +546,15 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
                     (RECV, spare[0], (r - 1) % G), (RECV, spare[1], (r - 1) % G)]
         if h >= 2:
             p_ops, got = _part_exchange(r, G, n, causal, zigzag, h - 1, send[(h - 1) % 2],
-                                        kernels, k, v, n_valid, grid)
+                                        recv, n_valid, grid)
             ops += p_ops
-            if got is not None:
-                received.append(got)
+            pending = got
         # every rank takes part in every exchange slot (a slot depends only on
         # h and G), even with no op of its own: keeps loopback/collective
         # transports in lockstep when causal hops are skipped
         slot = h < G - 1 or h >= 2
         if slot:
-            S.comm_wait(prev)
+            S.comm_wait(ready)
             if recorder is not None:
                 recorder.count_send("backward", ops)
                 recorder.mark(h, "send_start", S.comm)
@@ -529,19 +562,22 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
             if recorder is not None:
                 recorder.mark(h, "send_end", S.comm)
                 recorder.mark(h, "recv_ready", S.comm)
-        prev = done
-        if slot:
             S.compute_after_comm()
         if h < G - 1:
             (cur_k, cur_v), spare = spare, (cur_k, cur_v)
             if spare[0] is k:
                 spare = None
+    parts_k, parts_v = [own[0]], [own[1]]
     if G > 1:
-        p_ops, got = _part_exchange(r, G, n, causal, zigzag, G - 1, send[(G - 1) % 2], kernels,
-                                    k, v, n_valid, grid)
-        if got is not None:
-            received.append(got)
-        S.comm_after_compute()
+        # homecoming of hop G-1's contribution, overlapped by the own block's last half
+        if recorder is not None:
+            recorder.mark(G, "compute_start", S.compute)
+        if pending:
+            kernels.accumulate(own, recv, k, stream=S.compute)
+        ready = S.compute_mark()
+        p_ops, got = _part_exchange(r, G, n, causal, zigzag, G - 1, send[(G - 1) % 2], recv,
+                                    n_valid, grid)
+        S.comm_wait(ready)
         if recorder is not None:
             recorder.count_send("backward", p_ops)
             recorder.mark(G, "send_start", S.comm)
@@ -549,40 +585,50 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
         if recorder is not None:
             recorder.mark(G, "send_end", S.comm)
             recorder.mark(G, "recv_ready", S.comm)
+        if own_last is not None:
+            kernels.bwd(own_last, q, k, v, dout, scale, st, own[0], own[1], accumulate=True,
+                        stream=S.compute)
+        if recorder is not None:
+            recorder.mark(G, "compute_end", S.compute)
         S.compute_after_comm()
-    parts_k = [own[0]] + [x[0] for x in received]
-    parts_v = [own[1]] + [x[1] for x in received]
+        if got:
+            parts_k.append(recv[0])
+            parts_v.append(recv[1])
     kernels.bwd_finalize(st, parts_k, parts_v, dq, dk, dv, stream=S.compute)
+    kernels.finish(st, check, stream=S.compute)
     return dq, dk, dv
 
 
 def _qpart_exchange(r: int, G: int, n: int, causal: bool, zigzag: bool, hop: int, send_buf,
-                    kernels, like_q, n_valid=None, grid=None):
+                    recv_buf, n_valid=None, grid=None):
     """Ops moving the dQ contribution computed at `hop` (for the visiting query
-    block) to that block's home rank, and receiving the one computed for ours."""
-    ops, recv_buf = [], None
+    block) to that block's home rank, and receiving into `recv_buf` the one
+    computed for ours.  Returns (ops, received?)."""
+    ops = []
     src = (r - hop) % G                        # origin of the query block I processed
     if not plan_hop(src, G, (src - r) % G, n, causal, zigzag, n_valid, grid).skip:
         ops.append((SEND, send_buf, src))
     c = (r + hop) % G                          # the rank that processed MY block at `hop`
-    if not plan_hop(r, G, (r - c) % G, n, causal, zigzag, n_valid, grid).skip:
-        recv_buf = kernels.dq_part(like_q)
+    got = not plan_hop(r, G, (r - c) % G, n, causal, zigzag, n_valid, grid).skip
+    if got:
         ops.append((RECV, recv_buf, c))
-    return ops, recv_buf
+    return ops, got
 
 
 def ring_backward_qtravel(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: bool,
                           transport, kernels, n_valid: int | None = None, recorder=None,
-                          grid=None):
+                          grid=None, check: str = "sync"):
     """One rank's backward pass with the REFERENCE's payload:
     the query-side record (Q, dO, lse/D statistics) travels the ring and K/V/dK/dV
     stay pinned (BackwardBody ring.py:65-83, backward_step ring.py:221-242,
     Alg. 2 of the paper).  The reference also carries the dQ accumulator in the
     body; here each hop's dQ contribution goes home one hop later instead (the
     lag sim.py:19-21 says a real system needs), so no transfer waits on a kernel
-    of the same hop.  Wire bytes per hop: 2·n·H·D·elem (Q, dO) + statistics
-    + an fp32 dQ contribution, vs K/V + fp32 dK/dV for ring_backward.
-    Returns (dq, dk, dv) in q's dtype."""
+    of the same hop, and is folded into the home dQ accumulator as soon as it
+    lands (O(1) buffers).  The own block runs in two query halves like
+    ring_backward, the second one overlapping the last dQ homecoming.  Wire bytes
+    per hop: 2·n·H·D·elem (Q, dO) + statistics + an fp32 dQ contribution, vs K/V +
+    fp32 dK/dV for ring_backward.  Returns (dq, dk, dv) in q's dtype."""
     B, n, H, D = q.shape
     G, r = transport.world, transport.rank
     S = _Streams(q.device)
@@ -592,18 +638,27 @@ def ring_backward_qtravel(q, k, v, o, lse, dout, scale: float, causal: bool, zig
     payload = [q, dout] + kernels.stats_tensors(st)      # the visiting query block
     spare = None
     send = [None, None]
-    received = []
+    recv = kernels.dq_recv(q) if G > 1 else None
+    pending = False
+    own_last = None
     first_kv = True
-    prev = S.compute_mark()
     for h in range(G):
         src = (r - h) % G
         plan = plan_hop(src, G, (src - r) % G, n, causal, zigzag, n_valid, grid)
+        if h == 0:
+            plan, own_last = split_own_hop(plan, n, G)
         if recorder is not None:
             recorder.mark(h, "compute_start", S.compute)
+        if pending:
+            kernels.accumulate_dq(st, recv, q, stream=S.compute)
+            pending = False
+        ready = S.compute_mark()
         if h == 0:
             vst = st                                     # own queries: own dQ accumulator
         else:
-            send[h % 2] = kernels.dq_part(q, stream=S.compute)
+            # zeroed on the compute stream: the buffer was last read by slot h-1's
+            # send, which the compute stream has waited for
+            send[h % 2] = kernels.dq_part(q, stream=S.compute, reuse=send[h % 2])
             vst = kernels.visiting_state(st, payload[2:], send[h % 2])
         if not plan.skip:
             kernels.bwd(plan, payload[0], k, v, payload[1], scale, vst, dk_acc, dv_acc,
@@ -611,7 +666,6 @@ def ring_backward_qtravel(q, k, v, o, lse, dout, scale: float, causal: bool, zig
             first_kv = False
         if recorder is not None:
             recorder.mark(h, "compute_end", S.compute)
-        done = S.compute_mark()
         ops = []
         if h < G - 1:
             if spare is None:
@@ -620,13 +674,12 @@ def ring_backward_qtravel(q, k, v, o, lse, dout, scale: float, causal: bool, zig
             ops += [(RECV, t, (r - 1) % G) for t in spare]
         if h >= 2:
             p_ops, got = _qpart_exchange(r, G, n, causal, zigzag, h - 1, send[(h - 1) % 2],
-                                         kernels, q, n_valid, grid)
+                                         recv, n_valid, grid)
             ops += p_ops
-            if got is not None:
-                received.append(got)
+            pending = got
         slot = h < G - 1 or h >= 2
         if slot:
-            S.comm_wait(prev)
+            S.comm_wait(ready)
             if recorder is not None:
                 recorder.count_send("backward", ops)
                 recorder.mark(h, "send_start", S.comm)
@@ -634,21 +687,21 @@ def ring_backward_qtravel(q, k, v, o, lse, dout, scale: float, causal: bool, zig
             if recorder is not None:
                 recorder.mark(h, "send_end", S.comm)
                 recorder.mark(h, "recv_ready", S.comm)
-        prev = done
-        if slot:
             S.compute_after_comm()
         if h < G - 1:
             payload, spare = spare, payload
             if spare[0] is q:
                 spare = None   # never receive into the caller's tensors
-    if first_kv:                                  # every hop skipped: no key is visible
-        kernels.zero_((dk_acc, dv_acc), stream=S.compute)
+    got = False
     if G > 1:
-        p_ops, got = _qpart_exchange(r, G, n, causal, zigzag, G - 1, send[(G - 1) % 2], kernels,
-                                     q, n_valid, grid)
-        if got is not None:
-            received.append(got)
-        S.comm_after_compute()
+        if recorder is not None:
+            recorder.mark(G, "compute_start", S.compute)
+        if pending:
+            kernels.accumulate_dq(st, recv, q, stream=S.compute)
+        ready = S.compute_mark()
+        p_ops, got = _qpart_exchange(r, G, n, causal, zigzag, G - 1, send[(G - 1) % 2], recv,
+                                     n_valid, grid)
+        S.comm_wait(ready)
         if recorder is not None:
             recorder.count_send("backward", p_ops)
             recorder.mark(G, "send_start", S.comm)
@@ -656,8 +709,18 @@ def ring_backward_qtravel(q, k, v, o, lse, dout, scale: float, causal: bool, zig
         if recorder is not None:
             recorder.mark(G, "send_end", S.comm)
             recorder.mark(G, "recv_ready", S.comm)
+        if own_last is not None:
+            kernels.bwd(own_last, q, k, v, dout, scale, st, dk_acc, dv_acc,
+                        accumulate=not first_kv, stream=S.compute)
+            first_kv = False
+        if recorder is not None:
+            recorder.mark(G, "compute_end", S.compute)
         S.compute_after_comm()
-    kernels.bwd_finalize_qtravel(st, received, dk_acc, dv_acc, dq, dk, dv, stream=S.compute)
+    if first_kv:                                  # every hop skipped: no key is visible
+        kernels.zero_((dk_acc, dv_acc), stream=S.compute)
+    kernels.bwd_finalize_qtravel(st, [recv] if got else [], dk_acc, dv_acc, dq, dk, dv,
+                                 stream=S.compute)
+    kernels.finish(st, check, stream=S.compute)
     return dq, dk, dv
 
 

@@ -32,10 +32,17 @@ class OracleKernels:
     def __init__(self):
         self.launches = 0
 
-    def fwd_state(self, q):
+    def fwd_state(self, q, running=True):
         B, n, H, D = q.shape
         return {"o": np.zeros((B, H, n, D)), "m": np.full((B, H, n), -np.inf),
                 "l": np.zeros((B, H, n))}
+
+    def finish(self, state, check, stream=None, where="BurstAttention"):
+        """The oracle raises its errors synchronously (MaskError / NonFiniteError)."""
+
+    def accumulate(self, acc_pair, part_pair, like, stream=None):
+        for a, p in zip(acc_pair, part_pair):
+            a += p
 
     def part(self, k):
         return torch.zeros(k.shape, dtype=torch.float64)
@@ -115,8 +122,17 @@ class OracleKernels:
     def visiting_state(self, st, stats, dq_part):
         return {"lse": stats[0].numpy(), "D": stats[1].numpy(), "dq": dq_part.numpy()}
 
-    def dq_part(self, q, stream=None):
+    def dq_part(self, q, stream=None, reuse=None):
+        if reuse is not None:
+            reuse.zero_()
+            return reuse
         return torch.zeros(tuple(q.shape), dtype=torch.float64)
+
+    def dq_recv(self, q):
+        return torch.empty(tuple(q.shape), dtype=torch.float64)
+
+    def accumulate_dq(self, st, part, like, stream=None):
+        st["dq"] += part.numpy()
 
     def bwd_finalize_qtravel(self, st, dq_parts, dk_acc, dv_acc, dq, dk, dv, stream=None):
         self.launches += 1
