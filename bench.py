@@ -123,13 +123,31 @@ class ClockSampler:
 
 # ----------------------------------------------------------------- CPU reference
 
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _stock_reference():
+    """The unmodified reference package (pip-installed into baseline/_ref), or None."""
+    if os.path.isdir(REF_PATH) and REF_PATH not in sys.path:
+        sys.path.insert(0, REF_PATH)
+    try:
+        from burstsim import local_attn, masking   # noqa: F401
+        from burstsim.linalg import Matrix, Vector  # noqa: F401
+        return local_attn
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def cpu_reference_sample(cfg, world: int, rows: int = 512):
-    """The reference's tiled algorithm (oracle port of local_forward_tiled +
-    local_backward, 128x128 tiles, fp32 = the reference's `single` precision)
-    on `rows` queries x all keys of one head; returns (seconds, extrapolation
-    factor to the whole global step)."""
+    """The reference's LAO kernels on `rows` query rows x ALL keys of one head, fwd+bwd:
+    the stock `burstsim.local_attn.local_forward_tiled` + `PartialAttn.finalize` +
+    `local_backward` (local_attn.py:207-289) from baseline/_ref when installed (kind
+    "reference"), else the oracle port of the same tiled algorithm (kind "port").
+    128x128 tiles (the reference's own default for d=128 fp32 is 2x2, TileSpec.
+    for_partition local_attn.py:44-58, which would take hours), fp32 (the reference's
+    "single" precision), global positions via row_offset / n_total.
+    Returns (seconds, extrapolation factor to the whole global step, kind)."""
     import numpy as np
-    from oracle import burst_oracle as orc
     N, d = cfg["seq"], cfg["d"]
     rng = np.random.default_rng(0)
     q = rng.standard_normal((rows, d), dtype=np.float32)
@@ -137,18 +155,35 @@ def cpu_reference_sample(cfg, world: int, rows: int = 512):
     v = rng.standard_normal((N, d), dtype=np.float32)
     do = rng.standard_normal((rows, d), dtype=np.float32)
     scale = d ** -0.5
-    qpos = np.arange(N - rows, N)     # last rows: a causal sample sees every key
-    kpos = np.arange(N)
+    r0 = N - rows                     # last rows: a causal sample sees every key
+    la = _stock_reference()
     t0 = time.perf_counter()
-    part = orc.local_forward_tiled(q, k, v, scale, 128, 128, qpos, kpos, cfg["causal"])
-    o, lse = part.finalize()
-    dst = (do * o).sum(1)
-    orc.local_backward(q, k, v, do, lse.astype(np.float32), dst.astype(np.float32), scale,
-                       128, 128, qpos, kpos, cfg["causal"])
+    if la is not None:
+        from burstsim.linalg import Matrix, Vector
+        from burstsim.masking import BlockMask
+        M = lambda a: Matrix.from_array(a, dtype=np.float32)
+        tiles = la.TileSpec(128, 128)
+        mask = BlockMask(causal=True) if cfg["causal"] else None
+        part = la.local_forward_tiled(M(q), M(k), M(v), scale, tiles, mask, row_offset=r0,
+                                      col_offset=0, n_total=N)
+        o, lse = part.finalize()
+        dst = Vector((do * o.array).sum(1), dtype=np.float32)
+        la.local_backward(M(q), M(k), M(v), M(do), lse, dst, scale, tiles, mask, row_offset=r0,
+                          col_offset=0, n_total=N)
+        kind = "reference"
+    else:
+        from oracle import burst_oracle as orc
+        qpos, kpos = np.arange(r0, N), np.arange(N)
+        part = orc.local_forward_tiled(q, k, v, scale, 128, 128, qpos, kpos, cfg["causal"])
+        o, lse = part.finalize()
+        dst = (do * o).sum(1)
+        orc.local_backward(q, k, v, do, lse.astype(np.float32), dst.astype(np.float32), scale,
+                           128, 128, qpos, kpos, cfg["causal"])
+        kind = "port"
     dt = time.perf_counter() - t0
     # whole step: batch * heads * N query rows (causal: half the pairs on average)
-    factor = cfg["batch"] * cfg["heads"] * N / rows * (0.5 if cfg["causal"] else 1.0)
-    return dt, factor
+    factor = cfg["batch"] * cfg["heads"] * N / rows * _density(cfg) * (0.5 if cfg["causal"] else 1.0)
+    return dt, factor, kind
 
 
 def cpu_threads():
@@ -159,31 +194,47 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
-def run_reference(args, cfg, rank):
+def config_dict(cfg, world: int, comm: str):
+    """The `config` object of both arms' JSON lines (identical by construction)."""
+    B, N, H, D, causal = cfg["batch"], cfg["seq"], cfg["heads"], cfg["d"], cfg["causal"]
+    zigzag = causal and world > 1
+    n = N // world
+    return {"workload": cfg["workload"], "seq": N, "heads": H, "head_dim": D, "batch": B,
+            "visible_fraction": _density(cfg) * (0.5 if causal else 1.0),
+            "causal": causal, "partition": "zigzag" if zigzag else "contiguous",
+            "parallelism": f"ring sp{world}", "comm": comm if world > 1 else None,
+            "l2": f"inputs larger than L2 ({B * n * H * D * 2 / 2**30:.2f} GiB per tensor per rank)"}
+
+
+def run_reference(args, cfg, rank, world):
     if rank != 0:
         return
     for _ in range(args.warmup):
-        cpu_reference_sample(cfg, args.gpus, args.ref_rows)
+        cpu_reference_sample(cfg, world, args.ref_rows)
     times = []
-    factor = 1.0
+    factor, kind = 1.0, "port"
     for _ in range(args.steps):
-        dt, factor = cpu_reference_sample(cfg, args.gpus, args.ref_rows)
+        dt, factor, kind = cpu_reference_sample(cfg, world, args.ref_rows)
         times.append(dt)
     t_step = statistics.mean(times) * factor
     tokens = cfg["batch"] * cfg["seq"] / t_step
-    sample = (f"{args.ref_rows} query rows x {cfg['seq']} keys x 1 head, fwd+bwd, 128x128 tiles, "
-              f"fp32; extrapolated x{factor:.0f} to the whole step")
+    what = ("stock burstsim.local_attn (baseline/_ref)" if kind == "reference"
+            else "oracle port of the reference's tiled kernels")
+    sample = (f"{args.ref_rows} query rows x {cfg['seq']} keys x 1 head per step, fwd+bwd, "
+              f"{what}, 128x128 tiles, fp32, {statistics.mean(times):.2f} s per sample; "
+              f"extrapolated x{factor:.0f} to the whole step")
     line = {"impl": "reference", "metric": METRIC, "value": tokens, "unit": "tokens/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_step * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": cfg["workload"], "seq": cfg["seq"], "heads": cfg["heads"],
-                       "head_dim": cfg["d"], "batch": cfg["batch"], "causal": cfg["causal"]},
+            "config": config_dict(cfg, world, args.comm),
+            "extrapolated": True, "sample_rows": args.ref_rows,
+            "sample_s_per_step": statistics.mean(times),
             "cpu_baseline": {"value": tokens, "unit": "tokens/s", "cores": cpu_threads(),
-                             "kind": "port", "sample": sample},
+                             "kind": kind, "sample": sample},
             "e2e": {"value": tokens, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
-            "tflops_per_gpu": _flops(cfg) / t_step / 1e12}
+            "tflops_per_gpu": _flops(cfg) / world / t_step / 1e12}
     print(json.dumps(line), flush=True)
 
 
@@ -455,12 +506,14 @@ def run_ours(args, cfg, rank, world, local_rank):
                                "flops_per_launch": fwd_fl, "traffic": traffic_fwd}
     cpu = None
     if world == 1 and not args.skip_cpu:
-        dt, factor = cpu_reference_sample(cfg, 1, args.ref_rows)
+        dt, factor, kind = cpu_reference_sample(cfg, 1, args.ref_rows)
         ct = dt * factor
-        cpu = {"value": B * N / ct, "unit": "tokens/s", "cores": cpu_threads(), "kind": "port",
-               "sample": f"{args.ref_rows} query rows x {N} keys x 1 head fwd+bwd (reference "
-                         f"tiled algorithm, numpy fp32) in {dt:.2f}s, extrapolated x{factor:.0f}",
-               "tflops": _flops(cfg) / ct / 1e12}
+        cpu = {"value": B * N / ct, "unit": "tokens/s", "cores": cpu_threads(), "kind": kind,
+               "sample": f"{args.ref_rows} query rows x {N} keys x 1 head fwd+bwd ("
+                         + ("stock burstsim.local_attn" if kind == "reference" else
+                            "oracle port of the reference tiled algorithm")
+                         + f", numpy fp32) in {dt:.2f}s, extrapolated x{factor:.0f}",
+               "extrapolated": True, "tflops": _flops(cfg) / ct / 1e12}
     comm = None
     if world > 1:
         from paper_2403_09347_b200.ring import ring_comm_bytes
@@ -473,12 +526,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded N(0,1) q/k/v/dO)",
-        "config": {"workload": cfg["workload"], "seq": N, "heads": H, "head_dim": D, "batch": B,
-                   "visible_fraction": _density(cfg) * (0.5 if causal else 1.0),
-                   "causal": causal, "partition": "zigzag" if zigzag else "contiguous",
-                   "parallelism": f"ring sp{world}", "comm": args.comm if world > 1 else None,
-                   "l2": "inputs larger than L2 "
-                   f"({tensor_bytes / 2**30:.2f} GiB per tensor per rank)"},
+        "config": config_dict(cfg, world, args.comm),
         "tflops_per_gpu": tflops_gpu, "tc_peak_frac": tflops_gpu / peak_sus,
         "tc_peak_frac_of_burst": tflops_gpu / peak_burst,
         "e2e": {"value": B * N / (e2e_ms / 1e3), "unit": "tokens/s",
@@ -501,7 +549,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-rows", type=int, default=512)
+    ap.add_argument("--ref-rows", type=int, default=256)
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--comm", default="nccl", choices=["nccl", "ce"],
                     help="ring transport at N>1: NCCL send/recv, or copy engines over CUDA IPC")
@@ -511,7 +559,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        run_reference(args, cfg, rank)
+        run_reference(args, cfg, rank, world)
         return
     import torch
     # Test hook: BURST_BENCH_ONE_GPU=1 puts every rank on device 0 (exercises the N > 1

@@ -284,7 +284,7 @@ def test_ring_memory_independent_of_world():
     n, H = 2048, 4
     kern = _default_kernels()
     per_rank = {}
-    for world in (2, 8):
+    for world in (4, 8):
         q, k, v, do = make_inputs(1, n * world, H, 128, seed=world)
         sh = [[shard(t, r, world, False) for r in range(world)] for t in (q, k, v, do)]
         fw = run_ranks(world, lambda rank, tr: ring_forward(sh[0][rank], sh[1][rank], sh[2][rank],
@@ -298,4 +298,6 @@ def test_ring_memory_independent_of_world():
         torch.cuda.synchronize()
         # loopback ranks share the device: the per-rank figure is the total / world
         per_rank[world] = (torch.cuda.max_memory_allocated() - base) / world
-    assert per_rank[8] <= 1.25 * per_rank[2], per_rank
+    # held G-1 parts would add 4 fp32 (dK, dV) pairs per rank from G=4 to G=8
+    pair = 2 * n * H * 128 * 4
+    assert per_rank[8] - per_rank[4] < pair, (per_rank, pair)
