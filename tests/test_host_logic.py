@@ -400,7 +400,13 @@ def test_bench_reference_arm_cpu():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["unit"] == "tokens/s" and d["value"] > 0
-    assert d["cpu_baseline"]["kind"] == "port" and d["e2e"]["h2d_bytes_per_step"] == 0
+    ref_installed = os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "burstsim"))
+    assert d["cpu_baseline"]["kind"] == ("reference" if ref_installed else "port")
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["extrapolated"] is True
+    # same config object as our arm's line (so the driver sees same_config)
+    sys.path.insert(0, ROOT)
+    import bench
+    assert d["config"] == bench.config_dict(bench.CONFIGS["c2"], 1, "nccl")
     env = dict(os.environ, RANK="1", WORLD_SIZE="2")
     out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=300)
     assert out.returncode == 0 and not out.stdout.strip()
