@@ -147,10 +147,19 @@ BURST_API int burst_tl_accumulate(int batch, int heads, int head_dim, int64_t n,
  * row with no visible key, bit 1: non-finite output).  Synchronises `stream`. */
 BURST_API int burst_read_flags(void* stream, int* flags_out);
 
-/* Ring transport over NCCL (libnccl.so.2 resolved at run time). */
+/* Ring transport over NCCL (libnccl.so.2 resolved at run time).  The communicator is
+ * non-blocking and watched: joining, and every posted exchange, must make progress
+ * within `timeout_s` seconds, otherwise the communicator is aborted (stuck NCCL
+ * kernels return) and this and every later call on the ring returns BURST_E_DEADLOCK
+ * (DeadlockError, sim.py:290-310); an asynchronous NCCL error gives BURST_E_NCCL. */
 BURST_API int burst_ring_unique_id(void* out_128_bytes);
 BURST_API int burst_ring_create(const void* unique_id_128_bytes, int rank, int world, int device,
-                      void** ring);
+                      double timeout_s, void** ring);
+/* Non-blocking health check: retires finished exchanges, reports how many were posted
+ * and completed, and returns the ring's failure code (0 while healthy). */
+BURST_API int burst_ring_poll(void* ring, uint64_t* posted, uint64_t* completed);
+/* Block until every posted exchange has completed on the device, or the ring fails. */
+BURST_API int burst_ring_wait(void* ring);
 /* Grouped send(send_to) + recv(recv_from) of `bytes` on `stream`. */
 BURST_API int burst_ring_exchange(void* ring, const void* send, void* recv, size_t bytes, int send_to,
                         int recv_from, void* stream);

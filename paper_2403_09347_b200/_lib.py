@@ -76,7 +76,11 @@ _SIGS = {
     "burst_event_destroy": ([_c_p], _c_i32),
     "burst_copy_async": ([_c_p, _c_p, _c_sz, _c_p], _c_i32),
     "burst_ring_unique_id": ([_c_p], _c_i32),
-    "burst_ring_create": ([_c_p, _c_i32, _c_i32, _c_i32, ctypes.POINTER(_c_p)], _c_i32),
+    "burst_ring_create": ([_c_p, _c_i32, _c_i32, _c_i32, ctypes.c_double, ctypes.POINTER(_c_p)],
+                          _c_i32),
+    "burst_ring_poll": ([_c_p, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)],
+                        _c_i32),
+    "burst_ring_wait": ([_c_p], _c_i32),
     "burst_ring_exchange": ([_c_p, _c_p, _c_p, _c_sz, _c_i32, _c_i32, _c_p], _c_i32),
     "burst_ring_sendrecv": ([_c_p, ctypes.POINTER(P2POp), _c_i32, _c_p], _c_i32),
     "burst_ring_destroy": ([_c_p], _c_i32),

@@ -36,7 +36,7 @@ def _default_kernels():
     return _kernels
 
 
-def _transport_for(group, comm: str = "nccl"):
+def _transport_for(group, comm: str = "nccl", deadlock_timeout: float | None = None):
     """Ring transport of `group`: "nccl" (NCCL send/recv kernels) or "ce" (zero-SM
     copy-engine pushes into CUDA-IPC mailboxes, ring.IpcTransport)."""
     import torch.distributed as dist
@@ -47,9 +47,10 @@ def _transport_for(group, comm: str = "nccl"):
         return SoloTransport()
     if comm not in ("nccl", "ce"):
         raise ConfigError(f"comm must be 'nccl' or 'ce', got {comm!r}")
-    key = (id(group), torch.cuda.current_device(), comm)
+    key = (id(group), torch.cuda.current_device(), comm, deadlock_timeout)
     if key not in _transports:
-        _transports[key] = NcclTransport(group) if comm == "nccl" else IpcTransport(group)
+        _transports[key] = (NcclTransport(group, timeout_s=deadlock_timeout) if comm == "nccl"
+                            else IpcTransport(group))
     return _transports[key]
 
 
@@ -82,7 +83,8 @@ class _BurstAttnFn(torch.autograd.Function):
 def burst_attn_func(q, k, v, causal: bool = False, softmax_scale: float | None = None,
                     group=None, zigzag: bool | None = None, valid_len: int | None = None, *,
                     bwd_payload: str = "kv", mask=None, comm: str = "nccl", check: str = "async",
-                    _transport=None, _kernels=None, _recorders=None):
+                    deadlock_timeout: float | None = None, _transport=None, _kernels=None,
+                    _recorders=None):
     """BurstAttention over the ranks of `group` (NCCL ring over NVLink).
 
     q, k, v: [batch, n_local, heads, head_dim] shards of the global sequence
@@ -103,6 +105,10 @@ def burst_attn_func(q, k, v, causal: bool = False, softmax_scale: float | None =
     NonFiniteError: a non-finite output) is read: "async" (default) raises at a later
     call once the pass has finished on the device, or in `check_errors()`, without
     stalling the host; "sync" raises at the end of each pass (synchronises); "off".
+    `deadlock_timeout`: seconds without any ring exchange completing before the NCCL
+    communicator is aborted and the pass raises DeadlockError (default
+    BURST_RING_TIMEOUT_S or 600; the reference's deadlock_timeout, sim.py:501-510).
+    Every exchange also carries a small header checked at pass end (RingDesyncError).
     `_recorders`: optional (forward, backward) trace.PassRecorder pair that
     records this rank's measured hop timeline and byte ledger.
     """
@@ -113,7 +119,8 @@ def burst_attn_func(q, k, v, causal: bool = False, softmax_scale: float | None =
     scale = default_scale(q.shape[-1]) if softmax_scale is None else float(softmax_scale)
     if not scale > 0:
         raise ShapeError(f"scale must be finite and positive, got {scale}")
-    transport = _transport if _transport is not None else _transport_for(group, comm)
+    transport = (_transport if _transport is not None
+                 else _transport_for(group, comm, deadlock_timeout))
     kernels = _kernels if _kernels is not None else _default_kernels()
     if zigzag is None:
         zigzag = bool(causal) and transport.world > 1
@@ -167,7 +174,8 @@ class PassResult:
 def run_ring_pass(q, k, v, world: int, causal: bool = False, softmax_scale: float | None = None,
                   dout=None, zigzag: bool | None = None, kernels=None,
                   pad: bool = False, trace: bool = False,
-                  bwd_payload: str = "kv", mask=None, check: str = "sync") -> PassResult:
+                  bwd_payload: str = "kv", mask=None, check: str = "sync",
+                  deadlock_timeout: float | None = None) -> PassResult:
     """Whole-ring forward (+ backward when `dout` is given) of GLOBAL tensors
     [batch, N, heads, head_dim] over `world` simulated devices on this GPU.
 
@@ -176,6 +184,8 @@ def run_ring_pass(q, k, v, world: int, causal: bool = False, softmax_scale: floa
     copies for the ring hand-off.  `trace=True` also returns the measured
     per-hop timeline and byte ledger of every device (`.trace`, a
     trace.PassTrace in the reference's ScheduleTrace / CommLedger schema).
+    `deadlock_timeout`: seconds a rank waits for its peers at an exchange before the
+    pass raises DeadlockError (the reference's deadlock_timeout, sim.py:501-510).
     """
     if world < 1:
         raise ConfigError(f"gpus must be a positive integer, got {world}")
@@ -224,7 +234,7 @@ def run_ring_pass(q, k, v, world: int, causal: bool = False, softmax_scale: floa
                 n_valid, recorder=rec_b[rank], grid=grid, check=check)
         return o, lse, g
 
-    res = run_ranks(world, one)
+    res = run_ranks(world, one, deadlock_timeout=deadlock_timeout)
     ptrace = None
     if trace:
         for rf, rb in zip(rec_f, rec_b):

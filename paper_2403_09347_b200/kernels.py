@@ -111,33 +111,34 @@ class _Pending:
 
     def __init__(self):
         self.lock = threading.Lock()
-        self.items = []      # (host int32 tensor, event, where)
+        self.items = []      # (host tensor, event, checker(host) -> raises)
 
     def add(self, flags: torch.Tensor, stream, where: str) -> None:
-        host = torch.empty(1, dtype=torch.int32, pin_memory=True)
+        self.add_check(flags, stream, lambda h: raise_for_flags(int(h[0]), where))
+
+    def add_check(self, dev: torch.Tensor, stream, checker) -> None:
+        """Copy `dev` to pinned host memory on `stream`; run checker(host) once it lands."""
+        host = torch.empty(dev.shape, dtype=dev.dtype, pin_memory=True)
         with torch.cuda.stream(stream) if stream is not None else _nullctx():
-            host.copy_(flags, non_blocking=True)
+            host.copy_(dev, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record()
         with self.lock:
-            self.items.append((host, ev, where))
+            self.items.append((host, ev, checker))
 
     def check(self, block: bool) -> None:
         with self.lock:
-            items, keep = self.items, []
-            self.items = []
-            bad = None
-            for host, ev, where in items:
+            items, keep, ready = self.items, [], []
+            for host, ev, checker in items:
                 if block:
                     ev.synchronize()
                 elif not ev.query():
-                    keep.append((host, ev, where))
+                    keep.append((host, ev, checker))
                     continue
-                if bad is None and int(host[0]) != 0:
-                    bad = (int(host[0]), where)
+                ready.append((host, checker))
             self.items = keep
-        if bad is not None:
-            raise_for_flags(*bad)
+        for host, checker in ready:   # raises the first error; the rest are dropped
+            checker(host)
 
 
 PENDING = _Pending()

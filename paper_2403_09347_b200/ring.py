@@ -94,7 +94,23 @@ class _Streams:
 # transports
 # ---------------------------------------------------------------------------
 
-class SoloTransport:
+class _TransportBase:
+    """Pass bookkeeping shared by the transports: `pass_seq` numbers this rank's passes
+    (every rank runs the same passes in the same order, like the reference's lockstep
+    rounds) and `finish` is the end-of-pass health check of the channel."""
+
+    pass_seq = 0
+
+    def next_pass(self) -> int:
+        self.pass_seq = (self.pass_seq + 1) % (1 << 30)
+        return self.pass_seq
+
+    def finish(self, check: str) -> None:
+        """Raise DeadlockError / NcclError for a failed channel ("sync": after waiting
+        for every posted exchange; "async": only what is already known)."""
+
+
+class SoloTransport(_TransportBase):
     rank, world = 0, 1
 
     def sendrecv(self, ops, stream):
@@ -102,10 +118,20 @@ class SoloTransport:
             raise RingDesyncError("a world of one rank has nobody to exchange with")
 
 
-class NcclTransport:
-    """NCCL communicator owned by libburst_b200.so (burst_ring_create)."""
+def ring_timeout_s() -> float:
+    """Progress horizon of a ring (DeadlockError after this long without any exchange
+    completing; BURST_RING_TIMEOUT_S, default 600 s)."""
+    import os
+    return float(os.environ.get("BURST_RING_TIMEOUT_S", "600"))
 
-    def __init__(self, group=None, device: torch.device | None = None):
+
+class NcclTransport(_TransportBase):
+    """NCCL communicator owned by libburst_b200.so (burst_ring_create): non-blocking,
+    watched by a per-ring thread that aborts it when no exchange makes progress within
+    `timeout_s` (DeadlockError, sim.py:290-310) or NCCL reports an asynchronous error."""
+
+    def __init__(self, group=None, device: torch.device | None = None,
+                 timeout_s: float | None = None):
         import torch.distributed as dist
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
@@ -118,8 +144,22 @@ class NcclTransport:
                                    group=group)
         uid = (ctypes.c_char * 128).from_buffer_copy(obj[0])
         handle = ctypes.c_void_p()
-        _lib.call("burst_ring_create", uid, self.rank, self.world, dev.index, ctypes.byref(handle))
+        self.timeout_s = float(timeout_s if timeout_s is not None else ring_timeout_s())
+        _lib.call("burst_ring_create", uid, self.rank, self.world, dev.index,
+                  ctypes.c_double(self.timeout_s), ctypes.byref(handle))
         self.handle = handle
+
+    def finish(self, check: str) -> None:
+        if check == "sync":
+            _lib.call("burst_ring_wait", self.handle)
+        elif check == "async":
+            _lib.call("burst_ring_poll", self.handle, None, None)
+
+    def progress(self) -> tuple[int, int]:
+        """(exchanges posted, exchanges completed) so far on this ring."""
+        a, b = ctypes.c_uint64(0), ctypes.c_uint64(0)
+        _lib.call("burst_ring_poll", self.handle, ctypes.byref(a), ctypes.byref(b))
+        return a.value, b.value
 
     def sendrecv(self, ops, stream):
         arr = (_lib.P2POp * len(ops))()
@@ -137,7 +177,7 @@ class NcclTransport:
             self.handle = None
 
 
-class IpcTransport:
+class IpcTransport(_TransportBase):
     """Zero-SM transport: each send is a copy-engine
     cudaMemcpyAsync into the receiver's CUDA-IPC mailbox (NVLink for peers on other
     GPUs), ordered by interprocess CUDA events; no SM is used, so the transfers
@@ -280,7 +320,7 @@ class IpcTransport:
         self.boxes, self.retired = {}, []
 
 
-class TorchDistTransport:
+class TorchDistTransport(_TransportBase):
     """torch.distributed P2P (gloo on CPU: the multi-process host-logic tests)."""
 
     def __init__(self, group=None):
@@ -326,7 +366,7 @@ class LoopbackHub:
         return LoopbackTransport(self, rank)
 
 
-class LoopbackTransport:
+class LoopbackTransport(_TransportBase):
     """One rank of a LoopbackHub: device-to-device copies on the comm stream,
     ordered with CUDA events exactly like a real send/recv (RingChannel,
     sim.py:281-313; DeadlockError on a stalled peer, sim.py:290-310)."""
@@ -395,6 +435,75 @@ class LoopbackTransport:
 # the hop loops
 # ---------------------------------------------------------------------------
 
+class SlotLog:
+    """Exchange headers of one pass: the reference's desync checks (RingDesyncError on
+    an unexpected payload count, origin or sequence, sim.py:570-574 and 622-631) on a
+    real ring.  In every exchange slot rank r also sends [pass, slot, r, origin] to
+    r+1 -- origin = the rank whose block the slot's rotating payload carries, -1 when
+    the slot rotates nothing -- and receives its predecessor's header into row `slot`
+    of a device log.  At pass end the log is compared with what the schedule implies,
+    so a rank that skipped, repeated or reordered an exchange, ran another pass, or
+    forwarded a block from the wrong origin raises RingDesyncError."""
+
+    def __init__(self, transport, device: torch.device, slots, origin_fn):
+        import numpy as np
+        G, r = transport.world, transport.rank
+        self.active = G > 1
+        if not self.active:
+            return
+        self.G, self.r = G, r
+        self.row = {slot: i for i, slot in enumerate(slots)}
+        pid = transport.next_pass()
+        mine = np.array([[pid, sl, r, origin_fn(r, sl)] for sl in slots], dtype=np.int32)
+        prev = (r - 1) % G
+        self.expected = np.array([[pid, sl, prev, origin_fn(prev, sl)] for sl in slots],
+                                 dtype=np.int32)
+        t = torch.from_numpy(mine)
+        if device.type == "cuda":
+            t = t.pin_memory().to(device, non_blocking=True)
+        self.send = t
+        self.log = torch.full((len(slots), 4), -2, dtype=torch.int32, device=device)
+        self.device = device
+
+    def ops(self, slot: int):
+        if not self.active:
+            return []
+        i = self.row[slot]
+        return [(SEND, self.send[i], (self.r + 1) % self.G),
+                (RECV, self.log[i], (self.r - 1) % self.G)]
+
+    def _check(self, got) -> None:
+        got = got.numpy() if hasattr(got, "numpy") else got
+        for i in range(len(self.expected)):
+            if tuple(got[i]) != tuple(self.expected[i]):
+                raise RingDesyncError(
+                    f"rank {self.r}: exchange slot {int(self.expected[i][1])} delivered header "
+                    f"(pass, slot, sender, origin) = {tuple(int(x) for x in got[i])}, expected "
+                    f"{tuple(int(x) for x in self.expected[i])}")
+
+    def finish(self, check: str, stream) -> None:
+        if not self.active or check == "off":
+            return
+        if self.device.type != "cuda" or check == "sync":
+            if stream is not None:
+                stream.synchronize()
+            self._check(self.log.cpu())
+        else:
+            from .kernels import PENDING
+            PENDING.add_check(self.log, stream, self._check)
+
+
+def _rotating(G: int):
+    """origin_fn of a pass whose payload rotates at slots h < G-1 (K/V, or Q/dO)."""
+    return lambda rank, h: (rank - h) % G if h < G - 1 else -1
+
+
+def backward_slots(G: int) -> list:
+    """Exchange slots of a backward pass: K/V rotation at h < G-1, contribution
+    homecoming (one hop late) at h >= 2, and the final homecoming slot G."""
+    return [h for h in range(G) if h < G - 1 or h >= 2] + ([G] if G > 1 else [])
+
+
 def ring_forward(q, k, v, scale: float, causal: bool, zigzag: bool, transport, kernels,
                  n_valid: int | None = None, recorder=None, grid=None, check: str = "sync"):
     """One rank's forward pass.  Returns (O [B,n,H,D], lse [B,H,n] natural log).
@@ -409,6 +518,7 @@ def ring_forward(q, k, v, scale: float, causal: bool, zigzag: bool, transport, k
     o = torch.empty_like(q)
     lse = torch.empty(B, H, n, dtype=torch.float32, device=q.device)
     state = kernels.fwd_state(q, running=G > 1)
+    slog = SlotLog(transport, q.device, list(range(G - 1)), _rotating(G))
     cur_k, cur_v = k, v
     spare = None
     finalized = False
@@ -440,7 +550,7 @@ def ring_forward(q, k, v, scale: float, causal: bool, zigzag: bool, transport, k
             if recorder is not None:
                 recorder.count_send("forward", ops)
                 recorder.mark(h, "send_start", S.comm)
-            transport.sendrecv(ops, S.comm)
+            transport.sendrecv(ops + slog.ops(h), S.comm)
             if recorder is not None:
                 recorder.mark(h, "send_end", S.comm)
                 recorder.mark(h, "recv_ready", S.comm)
@@ -454,6 +564,8 @@ def ring_forward(q, k, v, scale: float, causal: bool, zigzag: bool, transport, k
     if not finalized:
         kernels.fwd_finalize(state, o, lse, stream=S.compute)
     kernels.finish(state, check, stream=S.compute)
+    slog.finish(check, S.compute)
+    transport.finish(check)
     return o, lse
 
 
@@ -507,6 +619,7 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
     st = kernels.bwd_prepare(o, dout, lse, stream=S.compute)
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     own = (kernels.part(k), kernels.part(v))
+    slog = SlotLog(transport, q.device, backward_slots(G), _rotating(G))
     send = [None, None]
     recv = (kernels.part(k), kernels.part(v)) if G > 1 else None
     pending = False              # `recv` holds a contribution not yet folded into `own`
@@ -558,7 +671,7 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
             if recorder is not None:
                 recorder.count_send("backward", ops)
                 recorder.mark(h, "send_start", S.comm)
-            transport.sendrecv(ops, S.comm)
+            transport.sendrecv(ops + slog.ops(h), S.comm)
             if recorder is not None:
                 recorder.mark(h, "send_end", S.comm)
                 recorder.mark(h, "recv_ready", S.comm)
@@ -581,7 +694,7 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
         if recorder is not None:
             recorder.count_send("backward", p_ops)
             recorder.mark(G, "send_start", S.comm)
-        transport.sendrecv(p_ops, S.comm)
+        transport.sendrecv(p_ops + slog.ops(G), S.comm)
         if recorder is not None:
             recorder.mark(G, "send_end", S.comm)
             recorder.mark(G, "recv_ready", S.comm)
@@ -596,6 +709,8 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
             parts_v.append(recv[1])
     kernels.bwd_finalize(st, parts_k, parts_v, dq, dk, dv, stream=S.compute)
     kernels.finish(st, check, stream=S.compute)
+    slog.finish(check, S.compute)
+    transport.finish(check)
     return dq, dk, dv
 
 
@@ -636,6 +751,7 @@ def ring_backward_qtravel(q, k, v, o, lse, dout, scale: float, causal: bool, zig
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     dk_acc, dv_acc = kernels.part(k), kernels.part(v)
     payload = [q, dout] + kernels.stats_tensors(st)      # the visiting query block
+    slog = SlotLog(transport, q.device, backward_slots(G), _rotating(G))
     spare = None
     send = [None, None]
     recv = kernels.dq_recv(q) if G > 1 else None
@@ -683,7 +799,7 @@ def ring_backward_qtravel(q, k, v, o, lse, dout, scale: float, causal: bool, zig
             if recorder is not None:
                 recorder.count_send("backward", ops)
                 recorder.mark(h, "send_start", S.comm)
-            transport.sendrecv(ops, S.comm)
+            transport.sendrecv(ops + slog.ops(h), S.comm)
             if recorder is not None:
                 recorder.mark(h, "send_end", S.comm)
                 recorder.mark(h, "recv_ready", S.comm)
@@ -705,7 +821,7 @@ def ring_backward_qtravel(q, k, v, o, lse, dout, scale: float, causal: bool, zig
         if recorder is not None:
             recorder.count_send("backward", p_ops)
             recorder.mark(G, "send_start", S.comm)
-        transport.sendrecv(p_ops, S.comm)
+        transport.sendrecv(p_ops + slog.ops(G), S.comm)
         if recorder is not None:
             recorder.mark(G, "send_end", S.comm)
             recorder.mark(G, "recv_ready", S.comm)
@@ -721,6 +837,8 @@ def ring_backward_qtravel(q, k, v, o, lse, dout, scale: float, causal: bool, zig
     kernels.bwd_finalize_qtravel(st, [recv] if got else [], dk_acc, dv_acc, dq, dk, dv,
                                  stream=S.compute)
     kernels.finish(st, check, stream=S.compute)
+    slog.finish(check, S.compute)
+    transport.finish(check)
     return dq, dk, dv
 
 
@@ -765,10 +883,13 @@ def _rank_streams(dev: int, rank: int):
         return _loopback_streams[key]
 
 
-def run_ranks(world: int, fn, timeout: float = 600.0) -> Sequence:
+def run_ranks(world: int, fn, timeout: float = 600.0,
+              deadlock_timeout: float | None = None) -> Sequence:
     """Run fn(rank, transport) for `world` loopback ranks in threads (the
-    reference's threaded executor, sim.py:575-620); re-raise the first error."""
-    hub = LoopbackHub(world)
+    reference's threaded executor, sim.py:575-620); re-raise the first error.
+    `deadlock_timeout`: seconds a rank may wait for its peers at an exchange before
+    the pass fails with DeadlockError (sim.py:290-310, 622-631)."""
+    hub = LoopbackHub(world, timeout=deadlock_timeout if deadlock_timeout is not None else 120.0)
     out = [None] * world
     errors = []
     dev = torch.cuda.current_device() if torch.cuda.is_available() else None
@@ -794,7 +915,9 @@ def run_ranks(world: int, fn, timeout: float = 600.0) -> Sequence:
     for t in threads:
         t.join(timeout)
     if errors:
-        raise errors[0]
+        # the first rank to fail names the cause; peers report the broken barrier
+        first = next((e for e in errors if not isinstance(e, DeadlockError)), errors[0])
+        raise first
     if any(t.is_alive() for t in threads):
         raise DeadlockError("ring ranks failed to finish")
     return out

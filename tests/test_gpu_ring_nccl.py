@@ -1,14 +1,22 @@
-"""GPU test of the NCCL ring transport behind the C ABI (burst_ring_*).
+"""GPU tests of the NCCL ring transport behind the C ABI (burst_ring_*).
 
-Only one GPU is available to the round, so the communicator has a single rank
-and every exchange is a send-to-self: this still runs the real NCCL grouped
-send/recv path that the multi-GPU ring uses, on a side stream.
+On a one-GPU box the communicator has a single rank and every exchange is a
+send-to-self (the real NCCL grouped send/recv path of the multi-GPU ring, on a side
+stream); the join-stall test shows the watchdog's DeadlockError; the torchrun test
+runs the whole ring through NcclTransport on 2, 4 and 8 GPUs and skips itself when
+fewer than 2 devices are visible.
 """
 
 import ctypes
+import os
+import subprocess
+import sys
+import textwrap
 
 import pytest
 import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 pytestmark = pytest.mark.gpu
 
@@ -19,7 +27,8 @@ def _one_rank_ring():
     uid = (ctypes.c_char * 128)()
     _lib.check(lib.burst_ring_unique_id(uid))
     h = ctypes.c_void_p()
-    _lib.check(lib.burst_ring_create(uid, 0, 1, torch.cuda.current_device(), ctypes.byref(h)))
+    _lib.check(lib.burst_ring_create(uid, 0, 1, torch.cuda.current_device(), 60.0,
+                                     ctypes.byref(h)))
     return lib, h
 
 
@@ -48,6 +57,10 @@ def test_nccl_self_exchange_grouped():
                                            ctypes.c_void_p(s.cuda_stream)))
         s.synchronize()
         assert torch.equal(rc, a)
+        _lib.check(lib.burst_ring_wait(h))
+        posted, done = ctypes.c_uint64(0), ctypes.c_uint64(0)
+        _lib.check(lib.burst_ring_poll(h, ctypes.byref(posted), ctypes.byref(done)))
+        assert posted.value == done.value == 2
     finally:
         lib.burst_ring_destroy(h)
 
@@ -62,3 +75,44 @@ def test_nccl_rejects_bad_peer():
             _lib.check(lib.burst_ring_sendrecv(h, ops, 1, ctypes.c_void_p(0)))
     finally:
         lib.burst_ring_destroy(h)
+
+
+def test_nccl_join_stall_raises_deadlock():
+    """Rank 0 of a 2-rank ring whose peer never joins: the non-blocking init is
+    abandoned after the timeout with BURST_E_DEADLOCK (DeadlockError) instead of
+    hanging (sim.py:290-310)."""
+    code = textwrap.dedent("""
+        import ctypes, sys, time
+        sys.path.insert(0, %r)
+        import torch
+        from paper_2403_09347_b200 import _lib
+        torch.cuda.init()
+        lib = _lib.load()
+        uid = (ctypes.c_char * 128)()
+        _lib.check(lib.burst_ring_unique_id(uid))
+        h = ctypes.c_void_p()
+        t0 = time.time()
+        rc = lib.burst_ring_create(uid, 0, 2, 0, 3.0, ctypes.byref(h))
+        print("RC", rc, round(time.time() - t0, 1), lib.burst_last_error().decode())
+    """ % ROOT)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=240)
+    line = [ln for ln in r.stdout.splitlines() if ln.startswith("RC")]
+    assert line, r.stdout + r.stderr
+    _, rc, secs = line[0].split()[:3]
+    assert int(rc) == 7, line[0]                    # BURST_E_DEADLOCK
+    assert float(secs) < 60, line[0]
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs for a real NCCL ring")
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_torchrun_nccl_ring_matches_oracle(world):
+    """burst_attn_func through NcclTransport (the bench's N > 1 transport) on `world`
+    GPUs: both backward payloads, contiguous and zigzag causal, against the oracle."""
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr", "127.0.0.1", "--master-port",
+           str(29600 + world), os.path.join(ROOT, "tests", "nccl_ring_worker.py")]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.count("RING_OK") == world, r.stdout[-3000:]
