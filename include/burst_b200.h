@@ -108,7 +108,10 @@ BURST_API int burst_fwd_finalize(int dtype, int batch, int heads, int head_dim, 
 /* Backward stats for every (b, h, row) of a [batch, n] query block, packed as
  * stats[0][B*H][ceil(n/128)*128] = lse * log2(e) and stats[1][...] = D =
  * rowsum(dout * o) (padded rows: +inf / 0); also zeroes dq_acc (TL) if given.
- * `stats` holds 2 * batch * heads * ceil(n/128) * 128 floats. */
+ * `stats` holds 2 * batch * heads * ceil(n/128) * 128 floats, followed by at least
+ * 128 floats of readable slack (any values) when burst_lao_bwd will see a
+ * query range that does not start on a 128-row tile: its tile loads then read up
+ * to 127 values past the last row. */
 BURST_API int burst_bwd_preprocess(int dtype, int batch, int heads, int head_dim, int64_t n, const void* o,
                          const void* dout, const float* lse, float* stats, float* dq_acc,
                          void* stream);

@@ -349,10 +349,15 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd_kernel(const __grid_const
         for (int j4 = 0; j4 < 16; ++j4) {
           const float4 Dv = dst4[half * 16 + j4];
           const int c = half * 64 + 4 * j4;
-          pk[2 * j4] = ptx::pack_bf16(pr[c] * (__uint_as_float(r[4 * j4]) - Dv.x),
-                                      pr[c + 1] * (__uint_as_float(r[4 * j4 + 1]) - Dv.y));
-          pk[2 * j4 + 1] = ptx::pack_bf16(pr[c + 2] * (__uint_as_float(r[4 * j4 + 2]) - Dv.z),
-                                          pr[c + 3] * (__uint_as_float(r[4 * j4 + 3]) - Dv.w));
+          // masked entries (P = 0) give dS = 0 exactly: a query tile that starts off the
+          // 128-row grid reads up to 127 lse/D values past the hop's last row (the next
+          // head's statistics, or past the end of the buffer for the last head), and
+          // 0 * (dP - garbage) must not turn into NaN
+          auto ds = [](float pv, float dp, float dd) { return pv != 0.f ? pv * (dp - dd) : 0.f; };
+          pk[2 * j4] = ptx::pack_bf16(ds(pr[c], __uint_as_float(r[4 * j4]), Dv.x),
+                                      ds(pr[c + 1], __uint_as_float(r[4 * j4 + 1]), Dv.y));
+          pk[2 * j4 + 1] = ptx::pack_bf16(ds(pr[c + 2], __uint_as_float(r[4 * j4 + 2]), Dv.z),
+                                          ds(pr[c + 3], __uint_as_float(r[4 * j4 + 3]), Dv.w));
         }
         // SW128 K-major: row t, 16-byte query chunk ch (8 bf16) of 128 B swizzle row
         uint8_t* rowp = sdS + half * 16384 + t * 128;

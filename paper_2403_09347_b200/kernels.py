@@ -67,6 +67,9 @@ def check_qkv(q, k, v) -> tuple[int, int, int, int]:
     return B, n, H, D
 
 
+STATS_SLACK = 128   # floats of readable slack after the backward stats (burst_bwd_preprocess)
+
+
 def ws_floats(B: int, H: int, D: int, n: int) -> int:
     return B * H * (-(-n // 128) * 128) * D
 
@@ -83,7 +86,7 @@ class FwdState:
 
 @dataclass
 class BwdState:
-    stats: torch.Tensor   # [2, B*H, ceil(n/128)*128]: lse*log2e, D
+    stats: torch.Tensor   # flat [2][B*H][ceil(n/128)*128] (lse*log2e, D) + STATS_SLACK
     dq_acc: torch.Tensor  # TL fp32
     flags: torch.Tensor   # [1] int32 error word of the pass
 
@@ -240,7 +243,13 @@ class CudaKernels:
         nt = -(-n // 128) * 128
         with torch.cuda.stream(stream) if stream is not None else _nullctx():
             flags = self._flags(o.device)
-        st = BwdState(torch.empty(2, B * H, nt, dtype=torch.float32, device=o.device),
+        # [2][B*H][nt] + STATS_SLACK zeroed floats: a query tile that starts off the
+        # 128-row grid (unaligned zigzag chunks) bulk-loads up to 127 values past the
+        # last row, which must stay inside the allocation (include/burst_b200.h)
+        stats = torch.empty(2 * B * H * nt + STATS_SLACK, dtype=torch.float32, device=o.device)
+        with torch.cuda.stream(stream) if stream is not None else _nullctx():
+            stats[2 * B * H * nt:].zero_()
+        st = BwdState(stats,
                       torch.empty(ws_floats(B, H, D, n), dtype=torch.float32, device=o.device),
                       flags)
         _lib.call("burst_bwd_preprocess", dtype_code(o), B, H, D, n, _ptr(o), _ptr(dout),

@@ -121,7 +121,13 @@ class GridMask:
         key = (str(device),)
         cache = _TABLES.setdefault(self, {})
         if key not in cache:
-            cache[key] = torch.from_numpy(self.table().reshape(-1).copy()).to(device)
+            t = torch.from_numpy(self.table().reshape(-1).copy()).to(device)
+            # the table is shared by every stream that launches with this mask (the rank
+            # threads of run_ring_pass each run on their own stream): the H2D copy was
+            # only ordered on the creating thread's stream, so finish it before any
+            # other stream can see the cached tensor
+            torch.cuda.current_stream(t.device).synchronize()
+            cache[key] = t
         return cache[key]
 
 

@@ -893,6 +893,9 @@ def run_ranks(world: int, fn, timeout: float = 600.0,
     out = [None] * world
     errors = []
     dev = torch.cuda.current_device() if torch.cuda.is_available() else None
+    # the caller produced the shards on its own stream (asynchronously); the rank
+    # streams are non-blocking, so they must wait for it before touching them
+    caller = torch.cuda.current_stream(dev) if dev is not None else None
 
     def work(rank):
         try:
@@ -900,6 +903,7 @@ def run_ranks(world: int, fn, timeout: float = 600.0,
                 torch.cuda.set_device(dev)
                 s, comm = _rank_streams(dev, rank)
                 _tls.streams = comm
+                s.wait_stream(caller)
                 with torch.cuda.stream(s):
                     out[rank] = fn(rank, hub.transport(rank))
                 s.synchronize()

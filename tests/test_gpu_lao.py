@@ -301,3 +301,44 @@ def test_ring_memory_independent_of_world():
     # held G-1 parts would add 4 fp32 (dK, dV) pairs per rank from G=4 to G=8
     pair = 2 * n * H * 128 * 4
     assert per_rank[8] - per_rank[4] < pair, (per_rank, pair)
+
+
+def test_unaligned_query_tile_ignores_stats_past_the_end():
+    """A backward hop whose query range starts off the 128-row grid (zigzag
+    Q_LATE_HALF) loads lse/D tiles that run up to 127 rows past the block's last
+    row; whatever lies there (here: NaN in the stats slack) must not reach dK
+    (0 * (dP - garbage) for masked entries).  Regression: flaky NonFiniteError in
+    test_bf16_grid_mask[q-768-2-True-True-spec1]."""
+    from paper_2403_09347_b200.kernels import CudaKernels, STATS_SLACK
+    from paper_2403_09347_b200.schedule import HopPlan, PosMap
+    B, n, H, D = 1, 384, 2, 128
+    q, k, v, do = make_inputs(B, n, H, D, seed=11)
+    scale = D ** -0.5
+    kern = CudaKernels()
+    full = HopPlan(0, 0, 0, "diag", 0, n, 0, n, False, PosMap(0, n, n), PosMap(0, n, n))
+    o = torch.empty_like(q)
+    lse = torch.empty(B, H, n, device="cuda")
+    kern.fwd(full, q, k, v, scale, kern.fwd_state(q, running=False), o, lse, first=True,
+             finalize=True)
+    st = kern.bwd_prepare(o, do, lse)
+    st.stats[-STATS_SLACK:] = float("nan")
+    late = HopPlan(0, 0, 0, "diag", 192, n - 192, 0, n, False, PosMap(0, n, n), PosMap(0, n, n))
+    dkp, dvp = kern.part(k), kern.part(v)
+    kern.bwd(late, q, k, v, do, scale, st, dkp, dvp, accumulate=False)
+    dk, dv = torch.empty_like(k), torch.empty_like(v)
+    kern.tl_sum([dkp], dk)
+    kern.tl_sum([dvp], dv)
+    torch.cuda.synchronize()
+    # fp64 reference of the same rectangle: rows [192, n) against every key
+    f = lambda t: t.double().cpu()[0]
+    qd, kd, vd, dod, od = f(q), f(k), f(v), f(do), f(o)
+    for h in range(H):
+        Q, K, V, dO = qd[192:, h], kd[:, h], vd[:, h], dod[192:, h]
+        L = lse.double().cpu()[0, h, 192:]
+        P = torch.exp(Q @ K.T * scale - L[:, None])
+        Dd = (dO * od[192:, h]).sum(-1)
+        dS = P * (dO @ V.T - Dd[:, None])
+        ref_dk, ref_dv = scale * dS.T @ Q, P.T @ dO
+        assert torch.isfinite(dk[0, :, h]).all()
+        assert max_abs(dk[0, :, h], ref_dk.numpy()) < BF16_TOL
+        assert max_abs(dv[0, :, h], ref_dv.numpy()) < BF16_TOL
