@@ -1,0 +1,19 @@
+"""Hidden-communication fractions of the measured loopback ring (trace.py), per
+world size and partition: one B200 runs every rank (threads), so kernels of
+different ranks share the GPU; the hidden fraction is what the schedule hides."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2403_09347_b200 import run_ring_pass
+from paper_2403_09347_b200.trace import comm_summary
+N, H, D = int(sys.argv[1]) if len(sys.argv) > 1 else 65536, 16, 128
+print(f"# exp/trace_ring_summary.py N={N} H={H} D={D} bf16, loopback ring on one B200")
+for G, causal in ((2, False), (4, False), (8, False), (4, True), (8, True)):
+    for payload in ("kv", "q"):
+        q, k, v, do = (torch.randn(1, N, H, D, device="cuda").to(torch.bfloat16) for _ in range(4))
+        run_ring_pass(q, k, v, G, causal=causal, dout=do, trace=True, bwd_payload=payload)
+        res = run_ring_pass(q, k, v, G, causal=causal, dout=do, trace=True, bwd_payload=payload)
+        f, b = comm_summary(res.trace.forward), comm_summary(res.trace.backward)
+        print(f"G={G} causal={causal!s:5} payload={payload}: fwd hidden {f['hidden_frac']:.3f} "
+              f"({f['send_us']:.0f} us sent) | bwd hidden {b['hidden_frac']:.3f} ({b['send_us']:.0f} us sent)",
+              flush=True)
