@@ -398,6 +398,13 @@ def run_ours(args, cfg, rank, world, local_rank):
                       / max(tot[0] / world, 1e-9) / 1e3,
                       "bwd_GBps_per_rank": recs[1].ledger.bytes_sent_backward
                       / max(tot[2] / world, 1e-9) / 1e3}
+        if args.comm == "ce":
+            # host time to post one exchange (device-side flags: no host round trip)
+            from paper_2403_09347_b200.api import _transport_for
+            hu = sorted(_transport_for(None, "ce").host_us)
+            if hu:
+                comm_trace["host_us_per_exchange_median"] = hu[len(hu) // 2]
+                comm_trace["host_us_per_exchange_max"] = hu[-1]
 
     # ---- e2e through the public API with pinned host buffers, as a training loop
     # would run it: step i's inputs are copied host->device while step i-1 computes

@@ -52,7 +52,8 @@ enum {
   BURST_E_CUDA = 5,
   BURST_E_NCCL = 6,
   BURST_E_DEADLOCK = 7,   /* DeadlockError */
-  BURST_E_UNSUPPORTED = 8
+  BURST_E_UNSUPPORTED = 8,
+  BURST_E_DESYNC = 9      /* RingDesyncError: an exchange that does not fit the ring's layout */
 };
 
 enum { BURST_DTYPE_BF16 = 0, BURST_DTYPE_F32 = 1 };
@@ -181,7 +182,8 @@ BURST_API int burst_ring_destroy(void* ring);
  * runtime pieces of a mailbox exchange.  Handles are opaque byte blobs of
  * burst_ipc_handle_bytes() bytes (mem and event handles have the same size). */
 BURST_API size_t burst_ipc_handle_bytes(void);
-/* Dedicated device allocation for a mailbox (an IPC handle names a whole allocation). */
+/* Dedicated, zeroed device allocation for a mailbox or flag array (an IPC handle
+ * names a whole allocation). */
 BURST_API int burst_ipc_alloc(size_t bytes, void** dev_ptr);
 BURST_API int burst_ipc_free(void* dev_ptr);
 BURST_API int burst_ipc_mem_handle(void* dev_ptr, void* out_handle);
@@ -190,6 +192,35 @@ BURST_API int burst_ipc_close_mem(void* dev_ptr);
 /* Interprocess event (timing disabled); its handle opens in another process. */
 BURST_API int burst_ipc_event_create(void** event, void* out_handle);
 BURST_API int burst_ipc_event_open(const void* handle, void** event);
+/* Device-side sequence flags of the IPC ring (no host round trip per exchange):
+ * burst_signal_u32 writes `value` into the local staging word `stage`, then copies
+ * it into `flag` (which may be IPC-mapped peer memory), both ordered after earlier
+ * work of `stream`; burst_wait_u32 blocks `stream` until the local `flag` reaches
+ * `value` (wrap-safe >=). */
+BURST_API int burst_signal_u32(void* stream, void* flag, void* stage, uint32_t value);
+BURST_API int burst_wait_u32(void* stream, void* flag, uint32_t value);
+/* The IPC ring's exchange engine (ring.IpcTransport): flags/stage are this rank's
+ * flag arrays ([world][2 slots][ready, free] uint32, zeroed), set_peer records the
+ * IPC-mapped flag array and mailbox of every peer, set_mailbox this rank's mailbox
+ * (2 slots of `slot_bytes`, split into tag regions of caps[0..2] bytes).  One
+ * exchange call: free-signal every sender, wait each receiver's free flag, push the
+ * SEND payloads into its slot regions (copy engines) and signal ready, wait every
+ * sender's ready flag, copy out the receives that are not already the mailbox
+ * region itself.  All ordered on `stream`; nothing blocks the host. */
+typedef struct {
+  void* buf;
+  size_t bytes;
+  int32_t peer;
+  int32_t is_send;
+  int32_t tag;       /* 0 rotating payload, 1 contribution, 2 exchange header */
+  int32_t pad_;
+} burst_ipc_op;
+BURST_API int burst_ipc_ring_create(int rank, int world, void* flags, void* stage, void** out);
+BURST_API int burst_ipc_ring_set_peer(void* ring, int peer, void* peer_flags, void* peer_mail);
+BURST_API int burst_ipc_ring_set_mailbox(void* ring, void* mail, size_t slot_bytes,
+                                         const uint64_t* caps);
+BURST_API int burst_ipc_ring_exchange(void* ring, const burst_ipc_op* ops, int nops, void* stream);
+BURST_API int burst_ipc_ring_destroy(void* ring);
 BURST_API int burst_event_record(void* event, void* stream);
 BURST_API int burst_stream_wait_event(void* stream, void* event);
 BURST_API int burst_event_destroy(void* event);

@@ -39,6 +39,12 @@ class Hop(ctypes.Structure):
                 ("grid_qcell", _c_i64), ("grid_kcell", _c_i64), ("flags", _c_p)]
 
 
+class IpcOp(ctypes.Structure):
+    """burst_ipc_op: one send or receive of an IPC-ring exchange (with its region tag)."""
+    _fields_ = [("buf", _c_p), ("bytes", _c_sz), ("peer", _c_i32), ("is_send", _c_i32),
+                ("tag", _c_i32), ("pad_", _c_i32)]
+
+
 class P2POp(ctypes.Structure):
     """burst_p2p: one send or receive of a grouped ring exchange."""
     _fields_ = [("buf", _c_p), ("bytes", _c_sz), ("peer", _c_i32), ("is_send", _c_i32)]
@@ -71,6 +77,13 @@ _SIGS = {
     "burst_ipc_close_mem": ([_c_p], _c_i32),
     "burst_ipc_event_create": ([ctypes.POINTER(_c_p), _c_p], _c_i32),
     "burst_ipc_event_open": ([_c_p, ctypes.POINTER(_c_p)], _c_i32),
+    "burst_signal_u32": ([_c_p, _c_p, _c_p, ctypes.c_uint32], _c_i32),
+    "burst_wait_u32": ([_c_p, _c_p, ctypes.c_uint32], _c_i32),
+    "burst_ipc_ring_create": ([_c_i32, _c_i32, _c_p, _c_p, ctypes.POINTER(_c_p)], _c_i32),
+    "burst_ipc_ring_set_peer": ([_c_p, _c_i32, _c_p, _c_p], _c_i32),
+    "burst_ipc_ring_set_mailbox": ([_c_p, _c_p, _c_sz, ctypes.POINTER(ctypes.c_uint64)], _c_i32),
+    "burst_ipc_ring_exchange": ([_c_p, _c_p, _c_i32, _c_p], _c_i32),
+    "burst_ipc_ring_destroy": ([_c_p], _c_i32),
     "burst_event_record": ([_c_p, _c_p], _c_i32),
     "burst_stream_wait_event": ([_c_p, _c_p], _c_i32),
     "burst_event_destroy": ([_c_p], _c_i32),

@@ -50,7 +50,7 @@ def _transport_for(group, comm: str = "nccl", deadlock_timeout: float | None = N
     key = (id(group), torch.cuda.current_device(), comm, deadlock_timeout)
     if key not in _transports:
         _transports[key] = (NcclTransport(group, timeout_s=deadlock_timeout) if comm == "nccl"
-                            else IpcTransport(group))
+                            else IpcTransport(group, timeout_s=deadlock_timeout))
     return _transports[key]
 
 

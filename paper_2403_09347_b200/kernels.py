@@ -297,10 +297,10 @@ class CudaKernels:
             buf.zero_()
         return buf
 
-    def dq_recv(self, q: torch.Tensor) -> torch.Tensor:
-        """Receive buffer for a dQ contribution (fully overwritten by the exchange)."""
+    def dq_like(self, q: torch.Tensor) -> torch.Tensor:
+        """Shape/dtype of a dQ contribution buffer (a meta tensor: no memory)."""
         B, n, H, D = q.shape
-        return torch.empty(ws_floats(B, H, D, n), dtype=torch.float32, device=q.device)
+        return torch.empty(ws_floats(B, H, D, n), dtype=torch.float32, device="meta")
 
     def accumulate_dq(self, st: BwdState, part: torch.Tensor, like: torch.Tensor,
                       stream=None) -> None:

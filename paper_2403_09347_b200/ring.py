@@ -38,6 +38,10 @@ from .errors import DeadlockError, RingDesyncError
 from .schedule import contributor_to, plan_hop
 
 SEND, RECV = "send", "recv"
+# op tags (optional 4th element of an op): the region of a mailbox transport's slot
+# the payload lands in (IpcTransport); other transports ignore them
+TAG_ROT, TAG_PART, TAG_HDR = 0, 1, 2
+HDR_BYTES = 16          # one SlotLog header: int32 [pass, slot, sender, origin]
 
 # ---------------------------------------------------------------------------
 # streams
@@ -100,6 +104,10 @@ class _TransportBase:
     rounds) and `finish` is the end-of-pass health check of the channel."""
 
     pass_seq = 0
+    mailbox = False     # True: receives land in transport-owned buffers handed out by rx()
+
+    def reserve(self, need: dict) -> None:
+        """Receive capacity per op tag for the coming pass (mailbox transports)."""
 
     def next_pass(self) -> int:
         self.pass_seq = (self.pass_seq + 1) % (1 << 30)
@@ -163,7 +171,7 @@ class NcclTransport(_TransportBase):
 
     def sendrecv(self, ops, stream):
         arr = (_lib.P2POp * len(ops))()
-        for i, (kind, t, peer) in enumerate(ops):
+        for i, (kind, t, peer, *_) in enumerate(ops):
             arr[i].buf = t.data_ptr()
             arr[i].bytes = t.numel() * t.element_size()
             arr[i].peer = peer
@@ -177,147 +185,197 @@ class NcclTransport(_TransportBase):
             self.handle = None
 
 
+class _DevBuf:
+    """__cuda_array_interface__ over a raw device range (torch.as_tensor views it)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (ptr, False), "version": 2}
+
+
 class IpcTransport(_TransportBase):
     """Zero-SM transport: each send is a copy-engine
-    cudaMemcpyAsync into the receiver's CUDA-IPC mailbox (NVLink for peers on other
-    GPUs), ordered by interprocess CUDA events; no SM is used, so the transfers
-    never compete with the full-grid LAO kernels the way NCCL send/recv kernels do.
+    cudaMemcpyAsync straight into the receiver's CUDA-IPC mailbox (NVLink for peers
+    on other GPUs); no SM is used, so transfers never compete with the full-grid LAO
+    kernels the way NCCL send/recv kernels do, and no host round trip happens per
+    exchange: ordering is carried by device-side sequence flags.
 
-    Per exchange (all ranks call it in lockstep, like the reference's rounds,
-    sim.py:551-574), with mailbox slot s alternating 0/1 (the DoubleBuffer of
-    sim.py:316-332):
-      1. capacity: every rank announces the bytes it will receive from each peer;
-         a mailbox too small is reallocated and its IPC handle re-shared
-         (all_gather_object; also the barrier that orders step 2 after the
-         receivers' step-4 records of two exchanges ago);
-      2. sender: comm stream waits the receiver's consumed[s] event, copies its
-         SEND tensors back to back into the receiver's mailbox[from me][s], then
-         records its own ready[s];
-      3. barrier (every ready[s] recorded before anyone waits on it);
-      4. receiver: waits the sender's ready[s], copies mailbox -> RECV tensors in
-         the same order, records consumed[s].
-    Host-side handshakes use `group` (gloo is enough).
-    """
+    Mailboxes: two slots (the DoubleBuffer of sim.py:316-332; exchange e uses slot
+    e % 2), each split into per-tag regions -- 0: the rotating payload (K/V, or Q/dO/
+    statistics), 1: a contribution going home, 2: exchange headers (SlotLog) -- sized
+    once per shape by `reserve` (every rank calls it with the same, shape-derived
+    sizes at pass start; only a growth is collective).  The ring engine receives IN
+    PLACE: `rx` hands out views of the next exchange's slot and the kernels read
+    them directly (no mailbox -> tensor copy).
 
-    def __init__(self, group=None, device: torch.device | None = None):
+    Exchange e, slot s, sequence q = e + 1, on the comm stream (which the engine has
+    already ordered after the compute that last read slot s):
+      1. for every peer p we receive from: flags_p[me][s].free = q (p may now
+         overwrite our slot s);
+      2. for every peer d we send to: wait flags_me[d][s].free >= q, push the SEND
+         tensors into d's slot s regions, then flags_d[me][s].ready = q;
+      3. for every peer p we receive from: wait flags_me[p][s].ready >= q.
+    Waits are cuStreamWaitValue32 on our own memory; signals a staged 4-byte copy
+    into the peer's flag array (burst_signal_u32).  A stalled peer stalls the comm
+    stream; `finish("sync")` then reports DeadlockError after the ring timeout."""
+
+    mailbox = True
+    TAGS = (0, 1, 2)
+
+    def __init__(self, group=None, device: torch.device | None = None,
+                 timeout_s: float | None = None):
         import torch.distributed as dist
         self.dist, self.group = dist, group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.timeout_s = float(timeout_s if timeout_s is not None else ring_timeout_s())
         lib = _lib.load()
+        self._exchange = lib.burst_ipc_ring_exchange
         self.hbytes = int(lib.burst_ipc_handle_bytes())
-        self.slot = 0
-        self.boxes = {}          # (src, slot) -> (device pointer, capacity): my mailboxes
-        self.peer_box = {}       # (dst, slot) -> (device pointer, capacity) in dst's memory
-        self.ready, self.consumed = [], []
-        handles = []
-        for _ in range(2):
-            for lst in (self.ready, self.consumed):
-                ev, h = ctypes.c_void_p(), (ctypes.c_char * self.hbytes)()
-                _lib.call("burst_ipc_event_create", ctypes.byref(ev), h)
-                lst.append(ev)
-                handles.append(bytes(h))
+        self.e = 0                       # exchanges posted so far (all ranks in lockstep)
+        self.caps = {t: 0 for t in self.TAGS}
+        self.mail, self.slot_bytes = None, 0     # my mailbox: 2 slots
+        self.peer_mail = {}              # peer -> base of its mailbox (IPC-mapped)
+        self.retired = []                # outgrown mailboxes (freed in close())
+        self.host_us = []                # host time to post each exchange (measurement)
+        self.c_us = []                   # ... of which inside burst_ipc_ring_exchange
+        # flags: [world][2 slots][ready, free] uint32 in my memory, written by peers;
+        # stage: the same shape, local staging words of the signals I send
+        n = self.world * 4 * 4
+        fl, st = ctypes.c_void_p(), ctypes.c_void_p()
+        _lib.call("burst_ipc_alloc", n, ctypes.byref(fl))
+        _lib.call("burst_ipc_alloc", n, ctypes.byref(st))
+        self.flags, self.stage = fl.value, st.value
+        ring = ctypes.c_void_p()
+        _lib.call("burst_ipc_ring_create", self.rank, self.world, fl, st, ctypes.byref(ring))
+        self.ring = ring
+        h = (ctypes.c_char * self.hbytes)()
+        _lib.call("burst_ipc_mem_handle", fl, h)
         allh = [None] * self.world
-        dist.all_gather_object(allh, handles, group=group)
-        self.peer_ready, self.peer_consumed = {}, {}
-        for r, hs in enumerate(allh):
-            if r == self.rank:
-                continue
-            for s in range(2):
-                for key, idx in ((self.peer_ready, 2 * s), (self.peer_consumed, 2 * s + 1)):
-                    ev = ctypes.c_void_p()
-                    buf = (ctypes.c_char * self.hbytes).from_buffer_copy(hs[idx])
-                    _lib.call("burst_ipc_event_open", buf, ctypes.byref(ev))
-                    key[(r, s)] = ev
-        self.started = set()     # slots whose consumed event has been recorded once
-        self.retired = []        # outgrown mailboxes (freed in close())
+        dist.all_gather_object(allh, bytes(h), group=group)
+        self.peer_flags = {}
+        for r, hb in enumerate(allh):
+            if r != self.rank:
+                self.peer_flags[r] = self._open(hb)
+                _lib.call("burst_ipc_ring_set_peer", self.ring, r,
+                          ctypes.c_void_p(self.peer_flags[r]), None)
+        self.last_wait = None            # event after the newest exchange
+        self._events = (torch.cuda.Event(), torch.cuda.Event())
+        self._arr = (_lib.IpcOp * 16)()
 
-    def _grow(self, needs: dict, s: int) -> dict:
-        """Reallocate my mailboxes that are too small; return {src: handle bytes}."""
-        out = {}
-        for src, nbytes in needs.items():
-            box = self.boxes.get((src, s))
-            if box is None or box[1] < nbytes:
-                cap = max(nbytes, 2 * box[1] if box is not None else 0)
-                if box is not None:   # the peer may still map it: freed in close()
-                    self.retired.append(box[0])
-                ptr = ctypes.c_void_p()
-                _lib.call("burst_ipc_alloc", cap, ctypes.byref(ptr))
-                self.boxes[(src, s)] = (ptr.value, cap)
-                h = (ctypes.c_char * self.hbytes)()
-                _lib.call("burst_ipc_mem_handle", ptr, h)
-                out[src] = (bytes(h), cap)
+    # ---------------------------------------------------------------- layout
+    def _open(self, hb: bytes) -> int:
+        ptr = ctypes.c_void_p()
+        buf = (ctypes.c_char * self.hbytes).from_buffer_copy(hb)
+        _lib.call("burst_ipc_open_mem", buf, ctypes.byref(ptr))
+        return ptr.value
+
+    def _off(self, tag: int) -> int:
+        return sum(self.caps[t] for t in self.TAGS if t < tag)
+
+    def reserve(self, need: dict) -> None:
+        """Make every tag region hold at least need[tag] bytes.  Called by every rank at
+        the same point of every pass with the same (shape-derived) sizes, so a growth
+        -- collective: device sync, barrier, reallocation, handle exchange -- happens
+        on all ranks together; otherwise this is a no-op."""
+        grow = {t: max(self.caps[t], -(-int(need.get(t, 0)) // 256) * 256) for t in self.TAGS}
+        if grow == self.caps and self.mail is not None:
+            return
+        torch.cuda.synchronize(self.device)
+        d = self.dist
+        d.barrier(group=self.group)            # no peer still pushes into the old slots
+        for ptr in self.peer_mail.values():
+            _lib.call("burst_ipc_close_mem", ctypes.c_void_p(ptr))
+        self.peer_mail = {}
+        if self.mail is not None:
+            self.retired.append(self.mail)     # views may still reference it
+        self.caps = grow
+        self.slot_bytes = max(sum(grow.values()), 256)
+        ptr = ctypes.c_void_p()
+        _lib.call("burst_ipc_alloc", 2 * self.slot_bytes, ctypes.byref(ptr))
+        self.mail = ptr.value
+        caps = (ctypes.c_uint64 * 3)(*[grow[t] for t in self.TAGS])
+        _lib.call("burst_ipc_ring_set_mailbox", self.ring, ptr, self.slot_bytes, caps)
+        h = (ctypes.c_char * self.hbytes)()
+        _lib.call("burst_ipc_mem_handle", ptr, h)
+        allh = [None] * self.world
+        d.all_gather_object(allh, bytes(h), group=self.group)
+        for r, hb in enumerate(allh):
+            if r != self.rank:
+                self.peer_mail[r] = self._open(hb)
+                _lib.call("burst_ipc_ring_set_peer", self.ring, r, None,
+                          ctypes.c_void_p(self.peer_mail[r]))
+
+    def rx(self, likes, tag: int) -> list:
+        """Receive buffers of the NEXT exchange for `likes` (in op order): views of our
+        mailbox slot, region `tag`; the pushes land there and the kernels read them."""
+        if self.mail is None:
+            raise RingDesyncError("IpcTransport.rx before reserve()")
+        base = self.mail + (self.e & 1) * self.slot_bytes + self._off(tag)
+        out, off = [], 0
+        for t in likes:
+            nb = t.numel() * t.element_size()
+            if off + nb > self.caps[tag]:
+                raise RingDesyncError(f"rank {self.rank}: receive of {off + nb} B exceeds the "
+                                      f"reserved tag-{tag} region ({self.caps[tag]} B)")
+            raw = torch.as_tensor(_DevBuf(base + off, nb), device=self.device)
+            out.append(raw.view(t.dtype).view(t.shape))
+            off += nb
         return out
 
+    # ---------------------------------------------------------------- exchange
     def sendrecv(self, ops, stream):
-        d, s = self.dist, self.slot
-        self.slot ^= 1
-        sh = ctypes.c_void_p(stream.cuda_stream)
-        needs = defaultdict(int)
-        for kind, t, peer in ops:
-            if kind == RECV:
-                needs[peer] += t.numel() * t.element_size()
-        # 1. capacity / handle exchange (+ the barrier of the protocol)
-        new = self._grow(needs, s)
-        allnew = [None] * self.world
-        d.all_gather_object(allnew, new, group=self.group)
-        for r, m in enumerate(allnew):
-            if r != self.rank and self.rank in m:
-                h, cap = m[self.rank]
-                old = self.peer_box.get((r, s))
-                if old is not None:
-                    _lib.call("burst_ipc_close_mem", ctypes.c_void_p(old[0]))
-                ptr = ctypes.c_void_p()
-                buf = (ctypes.c_char * self.hbytes).from_buffer_copy(h)
-                _lib.call("burst_ipc_open_mem", buf, ctypes.byref(ptr))
-                self.peer_box[(r, s)] = (ptr.value, cap)
-        # 2. pushes into the receivers' mailboxes (copy engines)
-        offs = defaultdict(int)
-        waited = set()
-        for kind, t, peer in ops:
-            if kind != SEND:
-                continue
-            if s in self.started and peer not in waited:
-                _lib.call("burst_stream_wait_event", sh, self.peer_consumed[(peer, s)])
-                waited.add(peer)
-            ptr, cap = self.peer_box[(peer, s)]
-            nb = t.numel() * t.element_size()
-            if offs[peer] + nb > cap:
-                raise RingDesyncError(f"rank {self.rank}: payload to {peer} exceeds its mailbox")
-            _lib.call("burst_copy_async", ctypes.c_void_p(ptr + offs[peer]),
-                      ctypes.c_void_p(t.data_ptr()), nb, sh)
-            offs[peer] += nb
-        _lib.call("burst_event_record", self.ready[s], sh)
-        # 3. every ready[s] recorded before anyone waits on it
-        d.barrier(group=self.group)
-        # 4. mailbox -> destination tensors
-        offs = defaultdict(int)
-        waited = set()
-        for kind, t, peer in ops:
-            if kind != RECV:
-                continue
-            if peer not in waited:
-                _lib.call("burst_stream_wait_event", sh, self.peer_ready[(peer, s)])
-                waited.add(peer)
-            box = self.boxes[(peer, s)][0]
-            nb = t.numel() * t.element_size()
-            _lib.call("burst_copy_async", ctypes.c_void_p(t.data_ptr()),
-                      ctypes.c_void_p(box + offs[peer]), nb, sh)
-            offs[peer] += nb
-        _lib.call("burst_event_record", self.consumed[s], sh)
-        self.started.add(s)
+        """Post one exchange (burst_ipc_ring_exchange: one C call, no host wait)."""
+        import time
+        t0 = time.perf_counter()
+        if len(ops) > len(self._arr):
+            self._arr = (_lib.IpcOp * (2 * len(ops)))()
+        arr = self._arr
+        for i, op in enumerate(ops):
+            t = op[1]
+            a = arr[i]
+            a.buf = t.data_ptr()
+            a.bytes = t.numel() * t.element_size()
+            a.peer = op[2]
+            a.is_send = 1 if op[0] == SEND else 0
+            a.tag = op[3] if len(op) > 3 else TAG_ROT
+        self.e += 1
+        t1 = time.perf_counter()
+        _lib.check(self._exchange(self.ring, arr, len(ops), ctypes.c_void_p(stream.cuda_stream)))
+        self.c_us.append((time.perf_counter() - t1) * 1e6)
+        ev = self._events[self.e & 1]
+        ev.record(stream)
+        self.last_wait = ev
+        self.host_us.append((time.perf_counter() - t0) * 1e6)
+
+    def finish(self, check: str) -> None:
+        """"sync": wait (bounded) for the newest exchange; a peer that never signals
+        leaves the comm stream blocked, reported as DeadlockError (sim.py:290-310)."""
+        if check != "sync" or self.last_wait is None:
+            return
+        import time
+        deadline = time.monotonic() + self.timeout_s
+        while not self.last_wait.query():
+            if time.monotonic() > deadline:
+                raise DeadlockError(f"rank {self.rank}: IPC ring exchange {self.e - 1} did not "
+                                    f"complete within {self.timeout_s:.0f} s")
+            time.sleep(1e-4)
 
     def close(self):
         lib = _lib.load()
         torch.cuda.synchronize(self.device)
-        for ptr, _ in self.peer_box.values():
+        for ptr in list(self.peer_mail.values()) + list(self.peer_flags.values()):
             lib.burst_ipc_close_mem(ctypes.c_void_p(ptr))
-        self.peer_box = {}
+        self.peer_mail, self.peer_flags = {}, {}
         self.dist.barrier(group=self.group)     # every peer unmapped before freeing
-        for ptr in [p for p, _ in self.boxes.values()] + self.retired:
+        mine = [self.mail] if self.mail is not None else []
+        for ptr in mine + self.retired + [self.flags, self.stage]:
             lib.burst_ipc_free(ctypes.c_void_p(ptr))
-        self.boxes, self.retired = {}, []
+        self.mail, self.retired = None, []
+        if self.ring:
+            lib.burst_ipc_ring_destroy(self.ring)
+            self.ring = None
 
 
 class TorchDistTransport(_TransportBase):
@@ -335,7 +393,7 @@ class TorchDistTransport(_TransportBase):
     def sendrecv(self, ops, stream):
         d = self.dist
         p2p = [d.P2POp(d.isend if kind == SEND else d.irecv, t, self._global(peer), self.group)
-               for kind, t, peer in ops]
+               for kind, t, peer, *_ in ops]
         if not p2p:
             return
         ctx = torch.cuda.stream(stream) if stream is not None else _nullctx()
@@ -386,7 +444,7 @@ class LoopbackTransport(_TransportBase):
         self.seq += 1
         cuda = stream is not None
         with hub.lock:
-            for kind, t, peer in ops:
+            for kind, t, peer, *_ in ops:
                 if kind == SEND:
                     ev = None
                     if cuda:
@@ -395,7 +453,7 @@ class LoopbackTransport(_TransportBase):
                     hub.box[(seq, self.rank, peer)].append((t, ev))
         self._sync()
         taken = defaultdict(int)
-        for kind, t, peer in ops:
+        for kind, t, peer, *_ in ops:
             if kind != RECV:
                 continue
             with hub.lock:
@@ -469,8 +527,8 @@ class SlotLog:
         if not self.active:
             return []
         i = self.row[slot]
-        return [(SEND, self.send[i], (self.r + 1) % self.G),
-                (RECV, self.log[i], (self.r - 1) % self.G)]
+        return [(SEND, self.send[i], (self.r + 1) % self.G, TAG_HDR),
+                (RECV, self.log[i], (self.r - 1) % self.G, TAG_HDR)]
 
     def _check(self, got) -> None:
         got = got.numpy() if hasattr(got, "numpy") else got
@@ -491,6 +549,23 @@ class SlotLog:
         else:
             from .kernels import PENDING
             PENDING.add_check(self.log, stream, self._check)
+
+
+def _nbytes(*ts) -> int:
+    return sum(t.numel() * t.element_size() for t in ts)
+
+
+def _recv_bufs(transport, likes, tag: int, spare, device=None):
+    """Receive targets of the next exchange: views of the transport's mailbox slot
+    (mailbox transports receive in place) or the engine's own buffers (`spare`,
+    allocated on first use and recycled by the caller).  `likes` give shape and
+    dtype (meta tensors allowed, with `device` naming where to allocate)."""
+    if transport.mailbox:
+        return list(transport.rx(likes, tag))
+    if spare is None:
+        spare = [torch.empty(t.shape, dtype=t.dtype, device=device if device is not None else t.device)
+                 for t in likes]
+    return list(spare)
 
 
 def _rotating(G: int):
@@ -519,6 +594,8 @@ def ring_forward(q, k, v, scale: float, causal: bool, zigzag: bool, transport, k
     lse = torch.empty(B, H, n, dtype=torch.float32, device=q.device)
     state = kernels.fwd_state(q, running=G > 1)
     slog = SlotLog(transport, q.device, list(range(G - 1)), _rotating(G))
+    if G > 1:
+        transport.reserve({TAG_ROT: _nbytes(k, v), TAG_HDR: HDR_BYTES})
     cur_k, cur_v = k, v
     spare = None
     finalized = False
@@ -542,11 +619,10 @@ def ring_forward(q, k, v, scale: float, causal: bool, zigzag: bool, transport, k
             recorder.mark(h, "compute_end", S.compute)
         done = S.compute_mark()
         if h < G - 1:
-            if spare is None:
-                spare = (torch.empty_like(k), torch.empty_like(v))
+            spare = _recv_bufs(transport, (k, v), TAG_ROT, spare)
             S.comm_wait(prev)
-            ops = [(SEND, cur_k, (r + 1) % G), (SEND, cur_v, (r + 1) % G),
-                   (RECV, spare[0], (r - 1) % G), (RECV, spare[1], (r - 1) % G)]
+            ops = [(SEND, cur_k, (r + 1) % G, TAG_ROT), (SEND, cur_v, (r + 1) % G, TAG_ROT),
+                   (RECV, spare[0], (r - 1) % G, TAG_ROT), (RECV, spare[1], (r - 1) % G, TAG_ROT)]
             if recorder is not None:
                 recorder.count_send("forward", ops)
                 recorder.mark(h, "send_start", S.comm)
@@ -593,11 +669,11 @@ def _part_exchange(r: int, G: int, n: int, causal: bool, zigzag: bool, hop: int,
     ops = []
     mine = plan_hop(r, G, hop, n, causal, zigzag, n_valid, grid)
     if not mine.skip:
-        ops += [(SEND, send_bufs[0], mine.src), (SEND, send_bufs[1], mine.src)]
+        ops += [(SEND, send_bufs[0], mine.src, TAG_PART), (SEND, send_bufs[1], mine.src, TAG_PART)]
     c = contributor_to(r, G, hop)
     theirs = plan_hop(c, G, hop, n, causal, zigzag, n_valid, grid)
     if not theirs.skip:
-        ops += [(RECV, recv_bufs[0], c), (RECV, recv_bufs[1], c)]
+        ops += [(RECV, recv_bufs[0], c, TAG_PART), (RECV, recv_bufs[1], c, TAG_PART)]
     return ops, not theirs.skip
 
 
@@ -620,8 +696,10 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     own = (kernels.part(k), kernels.part(v))
     slog = SlotLog(transport, q.device, backward_slots(G), _rotating(G))
+    if G > 1:
+        transport.reserve({TAG_ROT: _nbytes(k, v), TAG_PART: _nbytes(*own), TAG_HDR: HDR_BYTES})
     send = [None, None]
-    recv = (kernels.part(k), kernels.part(v)) if G > 1 else None
+    recv = None                  # contribution receive buffers (engine-owned or mailbox views)
     pending = False              # `recv` holds a contribution not yet folded into `own`
     own_last = None              # second query half of the own block (after hop G-1)
     cur_k, cur_v = k, v
@@ -653,11 +731,11 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
             recorder.mark(h, "compute_end", S.compute)
         ops = []
         if h < G - 1:
-            if spare is None:
-                spare = (torch.empty_like(k), torch.empty_like(v))
-            ops += [(SEND, cur_k, (r + 1) % G), (SEND, cur_v, (r + 1) % G),
-                    (RECV, spare[0], (r - 1) % G), (RECV, spare[1], (r - 1) % G)]
+            spare = _recv_bufs(transport, (k, v), TAG_ROT, spare)
+            ops += [(SEND, cur_k, (r + 1) % G, TAG_ROT), (SEND, cur_v, (r + 1) % G, TAG_ROT),
+                    (RECV, spare[0], (r - 1) % G, TAG_ROT), (RECV, spare[1], (r - 1) % G, TAG_ROT)]
         if h >= 2:
+            recv = _recv_bufs(transport, own, TAG_PART, recv)
             p_ops, got = _part_exchange(r, G, n, causal, zigzag, h - 1, send[(h - 1) % 2],
                                         recv, n_valid, grid)
             ops += p_ops
@@ -688,6 +766,7 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
         if pending:
             kernels.accumulate(own, recv, k, stream=S.compute)
         ready = S.compute_mark()
+        recv = _recv_bufs(transport, own, TAG_PART, recv)
         p_ops, got = _part_exchange(r, G, n, causal, zigzag, G - 1, send[(G - 1) % 2], recv,
                                     n_valid, grid)
         S.comm_wait(ready)
@@ -722,11 +801,11 @@ def _qpart_exchange(r: int, G: int, n: int, causal: bool, zigzag: bool, hop: int
     ops = []
     src = (r - hop) % G                        # origin of the query block I processed
     if not plan_hop(src, G, (src - r) % G, n, causal, zigzag, n_valid, grid).skip:
-        ops.append((SEND, send_buf, src))
+        ops.append((SEND, send_buf, src, TAG_PART))
     c = (r + hop) % G                          # the rank that processed MY block at `hop`
     got = not plan_hop(r, G, (r - c) % G, n, causal, zigzag, n_valid, grid).skip
     if got:
-        ops.append((RECV, recv_buf, c))
+        ops.append((RECV, recv_buf, c, TAG_PART))
     return ops, got
 
 
@@ -752,9 +831,13 @@ def ring_backward_qtravel(q, k, v, o, lse, dout, scale: float, causal: bool, zig
     dk_acc, dv_acc = kernels.part(k), kernels.part(v)
     payload = [q, dout] + kernels.stats_tensors(st)      # the visiting query block
     slog = SlotLog(transport, q.device, backward_slots(G), _rotating(G))
+    if G > 1:
+        dq_like = kernels.dq_like(q)         # shape/dtype of a dQ contribution (meta)
+        transport.reserve({TAG_ROT: _nbytes(*payload), TAG_PART: _nbytes(dq_like),
+                           TAG_HDR: HDR_BYTES})
     spare = None
     send = [None, None]
-    recv = kernels.dq_recv(q) if G > 1 else None
+    recv = None                  # dQ contribution receive buffer (engine-owned or a mailbox view)
     pending = False
     own_last = None
     first_kv = True
@@ -784,11 +867,12 @@ def ring_backward_qtravel(q, k, v, o, lse, dout, scale: float, causal: bool, zig
             recorder.mark(h, "compute_end", S.compute)
         ops = []
         if h < G - 1:
-            if spare is None:
-                spare = [torch.empty_like(t) for t in payload]
-            ops += [(SEND, t, (r + 1) % G) for t in payload]
-            ops += [(RECV, t, (r - 1) % G) for t in spare]
+            spare = _recv_bufs(transport, payload, TAG_ROT, spare)
+            ops += [(SEND, t, (r + 1) % G, TAG_ROT) for t in payload]
+            ops += [(RECV, t, (r - 1) % G, TAG_ROT) for t in spare]
         if h >= 2:
+            recv = _recv_bufs(transport, (dq_like,), TAG_PART,
+                              None if recv is None else (recv,), q.device)[0]
             p_ops, got = _qpart_exchange(r, G, n, causal, zigzag, h - 1, send[(h - 1) % 2],
                                          recv, n_valid, grid)
             ops += p_ops
@@ -815,6 +899,8 @@ def ring_backward_qtravel(q, k, v, o, lse, dout, scale: float, causal: bool, zig
         if pending:
             kernels.accumulate_dq(st, recv, q, stream=S.compute)
         ready = S.compute_mark()
+        recv = _recv_bufs(transport, (dq_like,), TAG_PART,
+                          None if recv is None else (recv,), q.device)[0]
         p_ops, got = _qpart_exchange(r, G, n, causal, zigzag, G - 1, send[(G - 1) % 2], recv,
                                      n_valid, grid)
         S.comm_wait(ready)

@@ -87,10 +87,10 @@ class PassRecorder:
             self.marks.append(_Mark(rnd, kind, None, time.perf_counter()))
 
     def count_send(self, phase: str, ops) -> None:
-        """Ledger entry for one exchange slot: `ops` = [(kind, tensor, peer)]."""
+        """Ledger entry for one exchange slot: `ops` = [(kind, tensor, peer[, tag])]."""
         from .ring import SEND
-        elems = sum(t.numel() for k, t, _ in ops if k == SEND)
-        nbytes = sum(t.numel() * t.element_size() for k, t, _ in ops if k == SEND)
+        elems = sum(t.numel() for k, t, *_ in ops if k == SEND)
+        nbytes = sum(t.numel() * t.element_size() for k, t, *_ in ops if k == SEND)
         if phase == "forward":
             self.ledger.elements_sent_forward += elems
             self.ledger.bytes_sent_forward += nbytes

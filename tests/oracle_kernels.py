@@ -128,8 +128,8 @@ class OracleKernels:
             return reuse
         return torch.zeros(tuple(q.shape), dtype=torch.float64)
 
-    def dq_recv(self, q):
-        return torch.empty(tuple(q.shape), dtype=torch.float64)
+    def dq_like(self, q):
+        return torch.empty(tuple(q.shape), dtype=torch.float64, device="meta")
 
     def accumulate_dq(self, st, part, like, stream=None):
         st["dq"] += part.numpy()

@@ -107,7 +107,7 @@ def test_exchange_headers_travel_in_every_slot():
         orig = transport.sendrecv
 
         def spy(ops, stream):
-            hdr = [t for kind, t, peer in ops if t.dtype == torch.int32]
+            hdr = [t for kind, t, peer, *_ in ops if t.dtype == torch.int32]
             seen.setdefault(rank, []).append(len(hdr))
             return orig(ops, stream)
         transport.sendrecv = spy
