@@ -331,7 +331,8 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     def step(qq, kk, vv, dd, recorders=None):
         o, lse = burst_attn_func(qq, kk, vv, causal=causal, zigzag=zigzag, _kernels=kern,
-                                 comm=args.comm, mask=cfg.get("mask"), _recorders=recorders)
+                                 comm=args.comm, mask=cfg.get("mask"), _recorders=recorders,
+                                 deterministic=args.deterministic)
         grads = torch.autograd.grad(o, (qq, kk, vv), dd)
         return o, grads
 
@@ -444,7 +445,8 @@ def run_ours(args, cfg, rank, world, local_rank):
             qq, kk, vv, dd = dbuf[i % 2]
             qq, kk, vv = (x.detach().requires_grad_(True) for x in (qq, kk, vv))
             o, lse = burst_attn_func(qq, kk, vv, causal=causal, zigzag=zigzag, _kernels=kern,
-                                     comm=args.comm, mask=cfg.get("mask"))
+                                     comm=args.comm, mask=cfg.get("mask"),
+                                     deterministic=args.deterministic)
             fwd_done = torch.cuda.Event()
             fwd_done.record(comp)
             d2h.wait_event(fwd_done)               # O leaves while the backward runs
@@ -533,7 +535,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded N(0,1) q/k/v/dO)",
-        "config": config_dict(cfg, world, args.comm),
+        "config": dict(config_dict(cfg, world, args.comm),
+                       **({"deterministic": True} if args.deterministic else {})),
         "tflops_per_gpu": tflops_gpu, "tc_peak_frac": tflops_gpu / peak_sus,
         "tc_peak_frac_of_burst": tflops_gpu / peak_burst,
         "e2e": {"value": B * N / (e2e_ms / 1e3), "unit": "tokens/s",
@@ -560,6 +563,8 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--comm", default="nccl", choices=["nccl", "ce"],
                     help="ring transport at N>1: NCCL send/recv, or copy engines over CUDA IPC")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="bit-reproducible backward (ordered dQ reductions)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))

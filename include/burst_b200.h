@@ -88,6 +88,12 @@ typedef struct {
    * key -> MaskError), bit 1 (non-finite output -> NonFiniteError), bit 2 (launch
    * could not run -> CudaError). */
   int32_t* flags;
+  /* Deterministic dQ (optional): device int32 array of batch * heads * ceil(n_q/128)
+   * words.  burst_lao_bwd zeroes it on the stream and then reduces every 128-row dQ
+   * tile in ascending key-tile order, so gradients are bit-reproducible run to run
+   * (the reference's bitwise executor equivalence, pkg/tests/test_sim.py:280-295).
+   * NULL = fastest (unordered fp32 reductions).  The f32 path is always ordered. */
+  int32_t* dq_order;
 } burst_hop;
 
 /* Elements (float) of one TL workspace for [batch, n, heads, head_dim]. */
@@ -109,10 +115,8 @@ BURST_API int burst_fwd_finalize(int dtype, int batch, int heads, int head_dim, 
 /* Backward stats for every (b, h, row) of a [batch, n] query block, packed as
  * stats[0][B*H][ceil(n/128)*128] = lse * log2(e) and stats[1][...] = D =
  * rowsum(dout * o) (padded rows: +inf / 0); also zeroes dq_acc (TL) if given.
- * `stats` holds 2 * batch * heads * ceil(n/128) * 128 floats, followed by at least
- * 128 floats of readable slack (any values) when burst_lao_bwd will see a
- * query range that does not start on a 128-row tile: its tile loads then read up
- * to 127 values past the last row. */
+ * `stats` holds 2 * batch * heads * ceil(n/128) * 128 floats (burst_lao_bwd reads
+ * whole 128-row tiles of the block, never past the last tile). */
 BURST_API int burst_bwd_preprocess(int dtype, int batch, int heads, int head_dim, int64_t n, const void* o,
                          const void* dout, const float* lse, float* stats, float* dq_acc,
                          void* stream);

@@ -57,13 +57,13 @@ def _transport_for(group, comm: str = "nccl", deadlock_timeout: float | None = N
 class _BurstAttnFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, q, k, v, scale, causal, zigzag, transport, kernels, n_valid, recorders,
-                bwd_payload, grid, check):
+                bwd_payload, grid, check, deterministic):
         rec_f, rec_b = recorders if recorders is not None else (None, None)
         o, lse = ring_forward(q, k, v, scale, causal, zigzag, transport, kernels, n_valid,
                               recorder=rec_f, grid=grid, check=check)
         ctx.save_for_backward(q, k, v, o, lse)
         ctx.cfg = (scale, causal, zigzag, transport, kernels, n_valid, rec_b, bwd_payload, grid,
-                   check)
+                   check, deterministic)
         ctx.mark_non_differentiable(lse)
         ctx.set_materialize_grads(False)     # no zero dlse tensor per backward
         return o, lse
@@ -71,20 +71,22 @@ class _BurstAttnFn(torch.autograd.Function):
     @staticmethod
     def backward(ctx, do, _dlse):
         q, k, v, o, lse = ctx.saved_tensors
-        scale, causal, zigzag, transport, kernels, n_valid, rec_b, bwd_payload, grid, check = ctx.cfg
+        (scale, causal, zigzag, transport, kernels, n_valid, rec_b, bwd_payload, grid, check,
+         deterministic) = ctx.cfg
         if do is None:
-            return (None,) * 13
+            return (None,) * 14
         bwd = ring_backward_qtravel if bwd_payload == "q" else ring_backward
         dq, dk, dv = bwd(q, k, v, o, lse, do.contiguous(), scale, causal, zigzag, transport,
-                         kernels, n_valid, recorder=rec_b, grid=grid, check=check)
-        return dq, dk, dv, None, None, None, None, None, None, None, None, None, None
+                         kernels, n_valid, recorder=rec_b, grid=grid, check=check,
+                         deterministic=deterministic)
+        return (dq, dk, dv) + (None,) * 11
 
 
 def burst_attn_func(q, k, v, causal: bool = False, softmax_scale: float | None = None,
                     group=None, zigzag: bool | None = None, valid_len: int | None = None, *,
                     bwd_payload: str = "kv", mask=None, comm: str = "nccl", check: str = "async",
-                    deadlock_timeout: float | None = None, _transport=None, _kernels=None,
-                    _recorders=None):
+                    deadlock_timeout: float | None = None, deterministic: bool = False,
+                    _transport=None, _kernels=None, _recorders=None):
     """BurstAttention over the ranks of `group` (NCCL ring over NVLink).
 
     q, k, v: [batch, n_local, heads, head_dim] shards of the global sequence
@@ -109,6 +111,9 @@ def burst_attn_func(q, k, v, causal: bool = False, softmax_scale: float | None =
     communicator is aborted and the pass raises DeadlockError (default
     BURST_RING_TIMEOUT_S or 600; the reference's deadlock_timeout, sim.py:501-510).
     Every exchange also carries a small header checked at pass end (RingDesyncError).
+    `deterministic`: reduce every dQ tile in ascending key-tile order so gradients are
+    bit-reproducible run to run and across transports (the reference's bitwise
+    executor equivalence, pkg/tests/test_sim.py:280-295); slower backward.
     `_recorders`: optional (forward, backward) trace.PassRecorder pair that
     records this rank's measured hop timeline and byte ledger.
     """
@@ -139,7 +144,8 @@ def burst_attn_func(q, k, v, causal: bool = False, softmax_scale: float | None =
         raise ConfigError(f"bwd_payload must be 'kv' or 'q', got {bwd_payload!r}")
     grid, causal = _bind_mask(mask, causal, q.shape[1] * transport.world, valid_len)
     return _BurstAttnFn.apply(q, k, v, scale, bool(causal), bool(zigzag), transport, kernels,
-                              valid_len, _recorders, bwd_payload, grid, check)
+                              valid_len, _recorders, bwd_payload, grid, check,
+                              bool(deterministic))
 
 
 def _bind_mask(mask, causal, total, n_valid=None):
@@ -175,7 +181,8 @@ def run_ring_pass(q, k, v, world: int, causal: bool = False, softmax_scale: floa
                   dout=None, zigzag: bool | None = None, kernels=None,
                   pad: bool = False, trace: bool = False,
                   bwd_payload: str = "kv", mask=None, check: str = "sync",
-                  deadlock_timeout: float | None = None) -> PassResult:
+                  deadlock_timeout: float | None = None,
+                  deterministic: bool = False) -> PassResult:
     """Whole-ring forward (+ backward when `dout` is given) of GLOBAL tensors
     [batch, N, heads, head_dim] over `world` simulated devices on this GPU.
 
@@ -186,6 +193,7 @@ def run_ring_pass(q, k, v, world: int, causal: bool = False, softmax_scale: floa
     trace.PassTrace in the reference's ScheduleTrace / CommLedger schema).
     `deadlock_timeout`: seconds a rank waits for its peers at an exchange before the
     pass raises DeadlockError (the reference's deadlock_timeout, sim.py:501-510).
+    `deterministic`: bit-reproducible backward (see burst_attn_func).
     """
     if world < 1:
         raise ConfigError(f"gpus must be a positive integer, got {world}")
@@ -231,7 +239,8 @@ def run_ring_pass(q, k, v, world: int, causal: bool = False, softmax_scale: floa
             return o, lse, None
         bwd = ring_backward_qtravel if bwd_payload == "q" else ring_backward
         g = bwd(qs, ks, vs, o, lse, do_sh[rank], scale, causal, zigzag, transport, kernels,
-                n_valid, recorder=rec_b[rank], grid=grid, check=check)
+                n_valid, recorder=rec_b[rank], grid=grid, check=check,
+                deterministic=deterministic)
         return o, lse, g
 
     res = run_ranks(world, one, deadlock_timeout=deadlock_timeout)

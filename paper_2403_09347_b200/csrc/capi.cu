@@ -16,7 +16,6 @@
 #include "../../include/burst_b200.h"
 #include "aux_kernels.cuh"
 #include "lao_bwd4_sm100.cuh"
-#include "lao_bwd_sm100.cuh"
 #include "lao_fwd_sm100.cuh"
 #include "simt_f32.cuh"
 
@@ -213,32 +212,6 @@ int launch_fwd_f32(const burst_hop* h, const void* q, const void* k, const void*
 }
 
 template <int D>
-int launch_bwd_bf16(const burst_hop* h, const void* q, const void* k, const void* v, const void* dout,
-                    const float* stats, float* dq_acc, float* dk, float* dv, int acc, cudaStream_t st) {
-  bwd::Params p;
-  memset(&p, 0, sizeof(p));
-  int rc;
-  if ((rc = make_tmap(&p.tm_q, q, h->n_q, h->heads, D, h->batch))) return rc;
-  if ((rc = make_tmap(&p.tm_do, dout, h->n_q, h->heads, D, h->batch))) return rc;
-  if ((rc = make_tmap(&p.tm_k, k, h->n_k, h->heads, D, h->batch))) return rc;
-  if ((rc = make_tmap(&p.tm_v, v, h->n_k, h->heads, D, h->batch))) return rc;
-  p.stats = stats; p.dq_acc = dq_acc; p.dk_acc = dk; p.dv_acc = dv;
-  p.hop = *h;
-  p.hop.flags = flags_of(h);
-  p.scale_log2 = h->softmax_scale * kLog2e;
-  p.scale = h->softmax_scale;
-  p.accumulate = acc;
-#ifdef BURST_TRACE
-  p.trace = trace_buffer();
-#endif
-  if ((rc = set_smem(bwd::lao_bwd_kernel<D>, bwd::Cfg<D>::kSmemBytes))) return rc;
-  dim3 grid((unsigned)ceil_div(h->k_len, bwd::BN), h->heads, h->batch);
-  bwd::lao_bwd_kernel<D><<<grid, bwd::kThreads, bwd::Cfg<D>::kSmemBytes, st>>>(p);
-  CHECK_LAUNCH();
-  return BURST_OK;
-}
-
-template <int D>
 int launch_bwd4_bf16(const burst_hop* h, const void* q, const void* k, const void* v, const void* dout,
                      const float* stats, float* dq_acc, float* dk, float* dv, int acc, cudaStream_t st) {
   bwd4::Params p;
@@ -254,16 +227,24 @@ int launch_bwd4_bf16(const burst_hop* h, const void* q, const void* k, const voi
   p.scale_log2 = h->softmax_scale * kLog2e;
   p.scale = h->softmax_scale;
   p.accumulate = acc;
+  p.dq_order = h->dq_order;
+  if (h->dq_order)
+    CUDA_TRY(cudaMemsetAsync(h->dq_order, 0, sizeof(int32_t) * (size_t)h->batch * h->heads *
+                                                 (size_t)ceil_div(h->n_q, bwd4::BM), st));
 #ifdef BURST_TRACE
   p.trace = trace_buffer();
 #endif
-  if ((rc = set_smem(bwd4::lao_bwd4_kernel<D, false>, bwd4::Cfg<D>::kSmemBytes))) return rc;
-  if ((rc = set_smem(bwd4::lao_bwd4_kernel<D, true>, bwd4::Cfg<D>::kSmemBytes))) return rc;
   dim3 grid((unsigned)ceil_div(h->k_len, bwd4::BN), h->heads, h->batch);
-  if (h->grid_skip)
-    bwd4::lao_bwd4_kernel<D, true><<<grid, bwd4::kThreads, bwd4::Cfg<D>::kSmemBytes, st>>>(p);
+  auto go = [&](auto kernel) -> int {
+    if (int e = set_smem(kernel, bwd4::Cfg<D>::kSmemBytes)) return e;
+    kernel<<<grid, bwd4::kThreads, bwd4::Cfg<D>::kSmemBytes, st>>>(p);
+    return BURST_OK;
+  };
+  if (h->dq_order)
+    rc = h->grid_skip ? go(bwd4::lao_bwd4_kernel<D, true, true>) : go(bwd4::lao_bwd4_kernel<D, false, true>);
   else
-    bwd4::lao_bwd4_kernel<D, false><<<grid, bwd4::kThreads, bwd4::Cfg<D>::kSmemBytes, st>>>(p);
+    rc = h->grid_skip ? go(bwd4::lao_bwd4_kernel<D, true, false>) : go(bwd4::lao_bwd4_kernel<D, false, false>);
+  if (rc) return rc;
   CHECK_LAUNCH();
   return BURST_OK;
 }
@@ -425,14 +406,11 @@ int burst_lao_bwd(const burst_hop* hop, const void* q, const void* k, const void
   }
   if (hop->k_len == 0) return BURST_OK;
   if (hop->dtype == BURST_DTYPE_BF16) {
-    // lao_bwd4 reduces whole 128-row dQ tiles: query ranges that do not start on a
-    // tile (unaligned zigzag chunks) take lao_bwd, which reduces row by row
-    const bool staged = hop->q_begin % 128 == 0;
+    // one kernel for every query range: lao_bwd4 walks whole 128-row dQ tiles of the
+    // block and masks the rows of the first tile before q_begin (unaligned zigzag chunks)
     if (hop->head_dim == 128)
-      return staged ? launch_bwd4_bf16<128>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st)
-                    : launch_bwd_bf16<128>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
-    return staged ? launch_bwd4_bf16<64>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st)
-                  : launch_bwd_bf16<64>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
+      return launch_bwd4_bf16<128>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
+    return launch_bwd4_bf16<64>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);
   }
   switch (hop->head_dim) {
     case 16: return launch_bwd_f32<16>(hop, q, k, v, dout, stats, dq_acc, dk_acc, dv_acc, accumulate, st);

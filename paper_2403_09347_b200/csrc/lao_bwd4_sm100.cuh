@@ -66,8 +66,24 @@ struct Params {
   burst_hop hop;
   float scale_log2, scale;
   int accumulate;
+  int* dq_order;      // deterministic mode: per-(b*h, query tile) count of finished key tiles
   long long* trace;   // BURST_TRACE builds only: per-iteration clock64 timeline
 };
+
+// Deterministic dQ: the reductions into one query tile happen in ascending key-tile
+// order.  Key tile j waits until dq_order[tile] == j, reduces, and publishes j + 1 once
+// its bulk reductions have completed (async-proxy writes ordered before the release).
+__device__ __forceinline__ void order_wait(const int* w, int want) {
+  int v;
+  do {
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(w) : "memory");
+  } while (v != want);
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ void order_publish(int* w, int val) {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(w), "r"(val) : "memory");
+}
 
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -89,7 +105,9 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 
 // kGrid: the hop carries a block-sparse grid mask (tile skipping + element masks);
 // the instantiation without it keeps the dense loops free of the skip bookkeeping.
-template <int D, bool kGrid>
+// kOrdered: deterministic dQ (p.dq_order set); its own instantiation keeps the turn
+// bookkeeping out of the drain's register budget in the default kernel.
+template <int D, bool kGrid, bool kOrdered>
 __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_constant__ Params p) {
   using C = Cfg<D>;
   // SW128 tiles need 1024-byte alignment; the declaration asks the compiler for it and
@@ -140,17 +158,23 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
   const int64_t NTq = ceil_div(hp.n_q, 128);
   const int64_t NTk = ceil_div(hp.n_k, 128);
 
-  // Query tiles touching this key tile: causal => suffix of the hop's queries.
-  int64_t qs = hp.q_begin;
+  // Query tiles touching this key tile, on the block's absolute 128-row grid (so every
+  // dQ tile is one contiguous TL run): causal => a suffix of the hop's queries.  Rows
+  // of the first tile before q_begin (unaligned zigzag chunks) or before the causal
+  // frontier are masked like causal columns.
+  int64_t qlo = hp.q_begin;
   if (hp.causal) {
     const int64_t first_q = count_le(hp.q_map, hp.n_q, pos_of(hp.k_map, k0) - 1);
-    if (first_q > qs) qs = hp.q_begin + ((first_q - hp.q_begin) / BM) * BM;
+    if (first_q > qlo) qlo = first_q;
   }
+  const int64_t qs = (qlo / BM) * BM;
   const int nq = qs < q_end ? (int)ceil_div(q_end - qs, BM) : 0;
   // Query-tile order rotated per CTA: concurrently resident CTAs (consecutive key
   // tiles of one head) reduce into different dQ tiles (measured best at 128K,
-  // profiles/r01_rotation_exp.txt).
-  const int rot = nq > 0 ? (int)((blockIdx.x * 7u) % (unsigned)nq) : 0;
+  // profiles/r01_rotation_exp.txt).  Deterministic mode walks the tiles in order
+  // (key tile j follows j - 1 through every tile).
+  constexpr bool ordered = kOrdered;
+  const int rot = (nq > 0 && !ordered) ? (int)((blockIdx.x * 7u) % (unsigned)nq) : 0;
   auto qtile = [&](int i) -> int64_t { int j = i + rot; if (j >= nq) j -= nq; return qs + (int64_t)j * BM; };
   // Block-sparse grid: query tiles whose every (query, key) pair with this CTA's keys
   // lies in skipped cells are skipped by every role.  Roles count LIVE tiles (stages,
@@ -158,8 +182,8 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
   const int64_t krows = (k0 + BN < k_end ? k0 + BN : k_end) - k0;
   auto live = [&](int i) -> bool {
     if (!kGrid) return true;
-    const int64_t q0 = qtile(i);
-    return grid_rect_live(hp, q0, (q0 + BM < q_end ? q0 + BM : q_end) - q0, k0, krows);
+    const int64_t q0 = qtile(i) < hp.q_begin ? hp.q_begin : qtile(i);
+    return grid_rect_live(hp, q0, (qtile(i) + BM < q_end ? qtile(i) + BM : q_end) - q0, k0, krows);
   };
   // The predicate is evaluated once per tile by the whole CTA into a SMEM bitmap (up to
   // kLiveWords * 32 tiles); every role then finds the next live tile with __ffs.
@@ -392,7 +416,8 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
     const int64_t krow = k0 + t;
     const bool kvalid = krow < k_end && krow < hp.n_k;
     const int64_t kpos = (hp.causal || kGrid) ? pos_of(hp.k_map, kvalid ? krow : k0) : 0;
-    const int64_t qfirst = hp.causal ? count_le(hp.q_map, hp.n_q, kpos - 1) : 0;
+    int64_t qfirst = hp.causal ? count_le(hp.q_map, hp.n_q, kpos - 1) : 0;
+    if (qfirst < hp.q_begin) qfirst = hp.q_begin;
     const float c2 = p.scale_log2;
     for (int i = 0, ti = next_live(0); i < nlive; ++i, ti = next_live(ti + 1)) {
       const int s = i & 1;
@@ -539,9 +564,20 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
     const int t = threadIdx.x & 127;           // query row within the tile
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     float4* stg = reinterpret_cast<float4*>(sStage);
+    // deterministic mode: this CTA's turn word of query tile u (walk index)
+    auto turn = [&](int u) -> int* { return p.dq_order + bh * NTq + qtile(u) / BM; };
+    const int me = (int)blockIdx.x;
+    int walked = 0;   // walk indices below this have been published (ordered mode)
     for (int i = 0, ti = next_live(0); i < nlive; ++i, ti = next_live(ti + 1)) {
       const int64_t q0 = qtile(ti);
-      const bool qvalid = q0 + t < q_end && q0 + t < hp.n_q;
+      const bool qvalid = q0 + t >= hp.q_begin && q0 + t < q_end && q0 + t < hp.n_q;
+      if (ordered && t == 0) {   // before the TMEM load: no tile registers live here
+        for (; walked < ti; ++walked) {   // grid-skipped tiles: pass the turn on
+          order_wait(turn(walked), me);
+          order_publish(turn(walked), me + 1);
+        }
+        order_wait(turn(ti), me);
+      }
       ptx::mbar_wait(dq_full, i & 1); BTRACE4(7, i);
       ptx::tc_fence_after();
       uint32_t r[D];
@@ -588,8 +624,18 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
           ptx::bulk_commit();
         }
       }
+      if (ordered && t == 0) {
+        ptx::bulk_wait_all();
+        order_publish(turn(ti), me + 1);
+        walked = ti + 1;
+      }
       BTRACE4(9, i);
     }
+    if (ordered && t == 0)
+      for (; walked < nq; ++walked) {
+        order_wait(turn(walked), me);
+        order_publish(turn(walked), me + 1);
+      }
     if (t == 0) ptx::bulk_wait_all();
   }
 

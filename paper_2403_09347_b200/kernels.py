@@ -89,6 +89,7 @@ class BwdState:
     stats: torch.Tensor   # flat [2][B*H][ceil(n/128)*128] (lse*log2e, D) + STATS_SLACK
     dq_acc: torch.Tensor  # TL fp32
     flags: torch.Tensor   # [1] int32 error word of the pass
+    order: torch.Tensor | None = None   # deterministic mode: burst_hop.dq_order words
 
 
 # bits of the device error word (include/burst_b200.h burst_hop.flags)
@@ -154,7 +155,7 @@ def check_errors() -> None:
 
 
 def make_hop(plan: HopPlan, q: torch.Tensor, k: torch.Tensor, scale: float,
-             flags: torch.Tensor | None = None) -> _lib.Hop:
+             flags: torch.Tensor | None = None, order: torch.Tensor | None = None) -> _lib.Hop:
     B, n_q, H, D = q.shape
     h = _lib.Hop()
     h.batch, h.heads, h.head_dim, h.dtype = B, H, D, dtype_code(q)
@@ -172,6 +173,8 @@ def make_hop(plan: HopPlan, q: torch.Tensor, k: torch.Tensor, scale: float,
         h.grid_qcell, h.grid_kcell = g.qcell, g.kcell
     if flags is not None:
         h.flags = flags.data_ptr()
+    if order is not None:
+        h.dq_order = order.data_ptr()
     return h
 
 
@@ -238,7 +241,9 @@ class CudaKernels:
             raise ValueError(f"check must be 'sync', 'async' or 'off', got {check!r}")
 
     # ------------------------------------------------------------ backward
-    def bwd_prepare(self, o, dout, lse, stream=None) -> BwdState:
+    def bwd_prepare(self, o, dout, lse, stream=None, deterministic: bool = False) -> BwdState:
+        """Backward stats + zeroed dQ accumulator of the pinned block; `deterministic`
+        also allocates the dQ turn words (bit-reproducible dQ reductions)."""
         B, n, H, D = o.shape
         nt = -(-n // 128) * 128
         with torch.cuda.stream(stream) if stream is not None else _nullctx():
@@ -249,16 +254,18 @@ class CudaKernels:
         stats = torch.empty(2 * B * H * nt + STATS_SLACK, dtype=torch.float32, device=o.device)
         with torch.cuda.stream(stream) if stream is not None else _nullctx():
             stats[2 * B * H * nt:].zero_()
+        order = (torch.empty(B * H * (-(-n // 128)), dtype=torch.int32, device=o.device)
+                 if deterministic else None)
         st = BwdState(stats,
                       torch.empty(ws_floats(B, H, D, n), dtype=torch.float32, device=o.device),
-                      flags)
+                      flags, order)
         _lib.call("burst_bwd_preprocess", dtype_code(o), B, H, D, n, _ptr(o), _ptr(dout),
                   _ptr(lse), _ptr(st.stats), _ptr(st.dq_acc), _stream_handle(stream))
         return st
 
     def bwd(self, plan: HopPlan, q, k, v, dout, scale: float, st: BwdState, dk_part, dv_part,
             accumulate: bool, stream=None) -> None:
-        hop = make_hop(plan, q, k, scale, st.flags)
+        hop = make_hop(plan, q, k, scale, st.flags, st.order)
         _lib.call("burst_lao_bwd", ctypes.byref(hop), _ptr(q), _ptr(k), _ptr(v), _ptr(dout),
                   _ptr(st.stats), _ptr(st.dq_acc), _ptr(dk_part), _ptr(dv_part), int(accumulate),
                   _stream_handle(stream))
@@ -285,7 +292,7 @@ class CudaKernels:
     def visiting_state(self, st: BwdState, stats: list, dq_part) -> BwdState:
         """Backward state of a visiting query block: its statistics, and the fresh
         dQ contribution buffer this hop reduces into."""
-        return BwdState(stats[0], dq_part, st.flags)
+        return BwdState(stats[0], dq_part, st.flags, st.order)
 
     def dq_part(self, q: torch.Tensor, stream=None, reuse: torch.Tensor | None = None) -> torch.Tensor:
         """A zeroed fp32 dQ contribution buffer (TL layout) for a visiting block,

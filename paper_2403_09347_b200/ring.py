@@ -679,7 +679,7 @@ def _part_exchange(r: int, G: int, n: int, causal: bool, zigzag: bool, hop: int,
 
 def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: bool, transport,
                   kernels, n_valid: int | None = None, recorder=None, grid=None,
-                  check: str = "sync"):
+                  check: str = "sync", deterministic: bool = False):
     """One rank's backward pass.  Returns (dq, dk, dv) in q's dtype.
 
     Contribution buffers are O(1) in the ring size: `own` accumulates this rank's
@@ -692,7 +692,7 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
     B, n, H, D = q.shape
     G, r = transport.world, transport.rank
     S = _Streams(q.device)
-    st = kernels.bwd_prepare(o, dout, lse, stream=S.compute)
+    st = kernels.bwd_prepare(o, dout, lse, stream=S.compute, deterministic=deterministic)
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     own = (kernels.part(k), kernels.part(v))
     slog = SlotLog(transport, q.device, backward_slots(G), _rotating(G))
@@ -811,7 +811,7 @@ def _qpart_exchange(r: int, G: int, n: int, causal: bool, zigzag: bool, hop: int
 
 def ring_backward_qtravel(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: bool,
                           transport, kernels, n_valid: int | None = None, recorder=None,
-                          grid=None, check: str = "sync"):
+                          grid=None, check: str = "sync", deterministic: bool = False):
     """One rank's backward pass with the REFERENCE's payload:
     the query-side record (Q, dO, lse/D statistics) travels the ring and K/V/dK/dV
     stay pinned (BackwardBody ring.py:65-83, backward_step ring.py:221-242,
@@ -826,7 +826,7 @@ def ring_backward_qtravel(q, k, v, o, lse, dout, scale: float, causal: bool, zig
     B, n, H, D = q.shape
     G, r = transport.world, transport.rank
     S = _Streams(q.device)
-    st = kernels.bwd_prepare(o, dout, lse, stream=S.compute)
+    st = kernels.bwd_prepare(o, dout, lse, stream=S.compute, deterministic=deterministic)
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     dk_acc, dv_acc = kernels.part(k), kernels.part(v)
     payload = [q, dout] + kernels.stats_tensors(st)      # the visiting query block
