@@ -94,6 +94,12 @@ typedef struct {
    * (the reference's bitwise executor equivalence, pkg/tests/test_sim.py:280-295).
    * NULL = fastest (unordered fp32 reductions).  The f32 path is always ordered. */
   int32_t* dq_order;
+  /* Key-tile visiting order of the bf16 forward (optional; local_forward_tiled's
+   * key_tile_order, local_attn.py:212-225): device int32 permutation of the hop's
+   * ceil(k_len/128) key tiles (128 keys each, counted from k_begin), read by every CTA
+   * (not validated on the device).  The online-softmax merge is order-independent up
+   * to rounding.  NULL = ascending.  The f32 path ignores it. */
+  const int32_t* key_order;
 } burst_hop;
 
 /* Elements (float) of one TL workspace for [batch, n, heads, head_dim]. */

@@ -145,7 +145,8 @@ def _block_partial(q, k, v, scale, allowed=None) -> Partial:
 
 
 def local_forward_tiled(q, k, v, scale, tile_rows=128, tile_cols=128,
-                        q_pos=None, k_pos=None, causal=False, grid=None) -> Partial:
+                        q_pos=None, k_pos=None, causal=False, grid=None,
+                        key_tile_order=None) -> Partial:
     """LAO forward over one (query block x key block) rectangle.
 
     Restates local_forward_tiled (local_attn.py:207-248): query tiles x key
@@ -153,17 +154,22 @@ def local_forward_tiled(q, k, v, scale, tile_rows=128, tile_cols=128,
     allowed entry is skipped (the SKIP decision, local_attn.py:151-155,
     masking.py:79-106).  ``q_pos``/``k_pos`` are global positions (the
     reference's row_offset/col_offset generalised to permuted shards).
+    ``key_tile_order`` permutes the key-tile visits (local_attn.py:212-225).
     """
     dt = q.dtype
     rows, d = q.shape
     out = Partial.empty(rows, v.shape[1], dt)
     if causal or grid is not None:
         assert q_pos is not None and k_pos is not None
+    k_edges = [(c0, min(c0 + tile_cols, k.shape[0])) for c0 in range(0, k.shape[0], tile_cols)]
+    order = list(range(len(k_edges))) if key_tile_order is None else list(key_tile_order)
+    if sorted(order) != list(range(len(k_edges))):
+        raise ValueError(f"key_tile_order must permute range({len(k_edges)})")
     for r0 in range(0, rows, tile_rows):
         r1 = min(r0 + tile_rows, rows)
         acc = Partial.empty(r1 - r0, v.shape[1], dt)
-        for c0 in range(0, k.shape[0], tile_cols):
-            c1 = min(c0 + tile_cols, k.shape[0])
+        for idx in order:
+            c0, c1 = k_edges[idx]
             allowed = None
             if causal or grid is not None:
                 allowed = mask_allowed(q_pos[r0:r1], k_pos[c0:c1], causal, grid)

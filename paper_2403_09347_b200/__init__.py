@@ -8,13 +8,14 @@ all compute goes through the C ABI in include/burst_b200.h.
 
 from .api import PassResult, burst_attn_func, run_ring_pass
 from .kernels import check_errors
+from .lao import local_backward, local_forward
 from .errors import (BurstSimError, ConfigError, CudaError, DeadlockError, MaskError,
                      MissingForwardError, NcclError, NonFiniteError, RingDesyncError, ShapeError,
                      UnsupportedError)
 from .schedule import HopPlan, plan_hop, shard, shard_map, unshard
 
 __all__ = [
-    "burst_attn_func", "run_ring_pass", "PassResult", "check_errors", "plan_hop", "HopPlan", "shard", "unshard",
+    "burst_attn_func", "run_ring_pass", "local_forward", "local_backward", "PassResult", "check_errors", "plan_hop", "HopPlan", "shard", "unshard",
     "shard_map", "BurstSimError", "ShapeError", "NonFiniteError", "MaskError", "ConfigError",
     "RingDesyncError", "DeadlockError", "MissingForwardError", "CudaError", "NcclError",
     "UnsupportedError",

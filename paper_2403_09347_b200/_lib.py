@@ -37,7 +37,7 @@ class Hop(ctypes.Structure):
                 ("q_map", PosMap), ("k_map", PosMap),
                 ("grid_skip", _c_p), ("grid_nqb", _c_i32), ("grid_nkb", _c_i32),
                 ("grid_qcell", _c_i64), ("grid_kcell", _c_i64), ("flags", _c_p),
-                ("dq_order", _c_p)]
+                ("dq_order", _c_p), ("key_order", _c_p)]
 
 
 class IpcOp(ctypes.Structure):

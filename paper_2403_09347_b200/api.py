@@ -57,13 +57,13 @@ def _transport_for(group, comm: str = "nccl", deadlock_timeout: float | None = N
 class _BurstAttnFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, q, k, v, scale, causal, zigzag, transport, kernels, n_valid, recorders,
-                bwd_payload, grid, check, deterministic):
+                bwd_payload, grid, check, deterministic, offset):
         rec_f, rec_b = recorders if recorders is not None else (None, None)
         o, lse = ring_forward(q, k, v, scale, causal, zigzag, transport, kernels, n_valid,
-                              recorder=rec_f, grid=grid, check=check)
+                              recorder=rec_f, grid=grid, check=check, offset=offset)
         ctx.save_for_backward(q, k, v, o, lse)
         ctx.cfg = (scale, causal, zigzag, transport, kernels, n_valid, rec_b, bwd_payload, grid,
-                   check, deterministic)
+                   check, deterministic, offset)
         ctx.mark_non_differentiable(lse)
         ctx.set_materialize_grads(False)     # no zero dlse tensor per backward
         return o, lse
@@ -72,21 +72,21 @@ class _BurstAttnFn(torch.autograd.Function):
     def backward(ctx, do, _dlse):
         q, k, v, o, lse = ctx.saved_tensors
         (scale, causal, zigzag, transport, kernels, n_valid, rec_b, bwd_payload, grid, check,
-         deterministic) = ctx.cfg
+         deterministic, offset) = ctx.cfg
         if do is None:
-            return (None,) * 14
+            return (None,) * 15
         bwd = ring_backward_qtravel if bwd_payload == "q" else ring_backward
         dq, dk, dv = bwd(q, k, v, o, lse, do.contiguous(), scale, causal, zigzag, transport,
                          kernels, n_valid, recorder=rec_b, grid=grid, check=check,
-                         deterministic=deterministic)
-        return (dq, dk, dv) + (None,) * 11
+                         deterministic=deterministic, offset=offset)
+        return (dq, dk, dv) + (None,) * 12
 
 
 def burst_attn_func(q, k, v, causal: bool = False, softmax_scale: float | None = None,
                     group=None, zigzag: bool | None = None, valid_len: int | None = None, *,
                     bwd_payload: str = "kv", mask=None, comm: str = "nccl", check: str = "async",
                     deadlock_timeout: float | None = None, deterministic: bool = False,
-                    _transport=None, _kernels=None, _recorders=None):
+                    start_offset: int = 0, _transport=None, _kernels=None, _recorders=None):
     """BurstAttention over the ranks of `group` (NCCL ring over NVLink).
 
     q, k, v: [batch, n_local, heads, head_dim] shards of the global sequence
@@ -114,6 +114,9 @@ def burst_attn_func(q, k, v, causal: bool = False, softmax_scale: float | None =
     `deterministic`: reduce every dQ tile in ascending key-tile order so gradients are
     bit-reproducible run to run and across transports (the reference's bitwise
     executor equivalence, pkg/tests/test_sim.py:280-295); slower backward.
+    `start_offset`: rank r starts the ring with the K/V block of rank r - start_offset
+    (mod G) instead of its own (initial_forward_body, ring.py:137-143); one extra
+    exchange, the merge order rotates and values agree to rounding.
     `_recorders`: optional (forward, backward) trace.PassRecorder pair that
     records this rank's measured hop timeline and byte ledger.
     """
@@ -145,7 +148,14 @@ def burst_attn_func(q, k, v, causal: bool = False, softmax_scale: float | None =
     grid, causal = _bind_mask(mask, causal, q.shape[1] * transport.world, valid_len)
     return _BurstAttnFn.apply(q, k, v, scale, bool(causal), bool(zigzag), transport, kernels,
                               valid_len, _recorders, bwd_payload, grid, check,
-                              bool(deterministic))
+                              bool(deterministic), _offset(start_offset))
+
+
+def _offset(start_offset) -> int:
+    """The reference takes any integer start offset modulo G (sim.py:414)."""
+    if isinstance(start_offset, bool) or not isinstance(start_offset, int):
+        raise ConfigError(f"start_offset must be an integer, got {start_offset!r}")
+    return start_offset
 
 
 def _bind_mask(mask, causal, total, n_valid=None):
@@ -182,7 +192,7 @@ def run_ring_pass(q, k, v, world: int, causal: bool = False, softmax_scale: floa
                   pad: bool = False, trace: bool = False,
                   bwd_payload: str = "kv", mask=None, check: str = "sync",
                   deadlock_timeout: float | None = None,
-                  deterministic: bool = False) -> PassResult:
+                  deterministic: bool = False, start_offset: int = 0) -> PassResult:
     """Whole-ring forward (+ backward when `dout` is given) of GLOBAL tensors
     [batch, N, heads, head_dim] over `world` simulated devices on this GPU.
 
@@ -194,12 +204,14 @@ def run_ring_pass(q, k, v, world: int, causal: bool = False, softmax_scale: floa
     `deadlock_timeout`: seconds a rank waits for its peers at an exchange before the
     pass raises DeadlockError (the reference's deadlock_timeout, sim.py:501-510).
     `deterministic`: bit-reproducible backward (see burst_attn_func).
+    `start_offset`: rotated initial K/V assignment (see burst_attn_func).
     """
     if world < 1:
         raise ConfigError(f"gpus must be a positive integer, got {world}")
     if bwd_payload not in ("kv", "q"):
         raise ConfigError(f"bwd_payload must be 'kv' or 'q', got {bwd_payload!r}")
     kernels = kernels if kernels is not None else _default_kernels()
+    offset = _offset(start_offset)
     if kernels.name == "cuda":
         check_qkv(q, k, v)
     if zigzag is None:
@@ -234,13 +246,13 @@ def run_ring_pass(q, k, v, world: int, causal: bool = False, softmax_scale: floa
     def one(rank, transport):
         qs, ks, vs = shards[0][rank], shards[1][rank], shards[2][rank]
         o, lse = ring_forward(qs, ks, vs, scale, causal, zigzag, transport, kernels, n_valid,
-                              recorder=rec_f[rank], grid=grid, check=check)
+                              recorder=rec_f[rank], grid=grid, check=check, offset=offset)
         if do_sh is None:
             return o, lse, None
         bwd = ring_backward_qtravel if bwd_payload == "q" else ring_backward
         g = bwd(qs, ks, vs, o, lse, do_sh[rank], scale, causal, zigzag, transport, kernels,
                 n_valid, recorder=rec_b[rank], grid=grid, check=check,
-                deterministic=deterministic)
+                deterministic=deterministic, offset=offset)
         return o, lse, g
 
     res = run_ranks(world, one, deadlock_timeout=deadlock_timeout)

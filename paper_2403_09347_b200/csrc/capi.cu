@@ -187,7 +187,7 @@ int launch_fwd_bf16(const burst_hop* h, const void* q, const void* k, const void
   if ((rc = set_smem(fwd::lao_fwd_kernel<D, false>, fwd::Cfg<D>::kSmemBytes))) return rc;
   if ((rc = set_smem(fwd::lao_fwd_kernel<D, true>, fwd::Cfg<D>::kSmemBytes))) return rc;
   dim3 grid((unsigned)ceil_div(h->q_len, 2 * fwd::BM), h->heads, h->batch);
-  if (h->grid_skip)
+  if (h->grid_skip || h->key_order)
     fwd::lao_fwd_kernel<D, true><<<grid, fwd::kThreads, fwd::Cfg<D>::kSmemBytes, st>>>(p);
   else
     fwd::lao_fwd_kernel<D, false><<<grid, fwd::kThreads, fwd::Cfg<D>::kSmemBytes, st>>>(p);

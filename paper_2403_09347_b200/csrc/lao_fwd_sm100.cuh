@@ -77,8 +77,11 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>(a + pad);
 }
 
-// kGrid: the hop carries a block-sparse grid mask (tile skipping + element masks);
-// the instantiation without it keeps the dense loops free of the skip bookkeeping.
+// kGrid: the general instantiation -- the hop carries a block-sparse grid mask (tile
+// skipping + element masks) and/or a key-tile visiting order (burst_hop.key_order,
+// local_forward_tiled's key_tile_order, local_attn.py:212-225); the dense instantiation
+// keeps its loops free of that bookkeeping.  Roles walk "visit" indices u; tile j =
+// key_order[u] (or u).
 template <int D, bool kGrid>
 __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_constant__ Params p) {
   using C = Cfg<D>;
@@ -118,11 +121,17 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
     if (kspan < 0) kspan = 0;
   }
   const int nkv = (int)ceil_div(kspan, BN);
+  // Visiting order: with key_order the walk covers every key tile of the hop and the
+  // ones past the causal span are skipped like grid-dead tiles.
+  const int32_t* korder = kGrid ? hp.key_order : nullptr;
+  const int nu = korder ? (int)ceil_div(hp.k_len, BN) : nkv;
+  auto tile_at = [&](int u) -> int { return korder ? __ldg(korder + u) : u; };
   // Block-sparse grid: KV tiles whose every (query, key) pair lies in skipped cells
   // are skipped by every role (each evaluates the same predicate).
   const int64_t qrows = (row0 + 2 * BM < q_end ? row0 + 2 * BM : q_end) - row0;
   auto live = [&](int j) -> bool {
     if (!kGrid) return true;
+    if (j >= nkv) return false;
     const int64_t kr = kspan - (int64_t)j * BN;
     return grid_rect_live(hp, row0, qrows, hp.k_begin + (int64_t)j * BN, kr < BN ? kr : BN);
   };
@@ -132,7 +141,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
   // per-row grid bits there.
   uint32_t* live_bits = reinterpret_cast<uint32_t*>(bars + 32);
   uint32_t* full_bits = live_bits + C::kLiveWords;
-  const bool use_bits = kGrid && nkv <= C::kLiveWords * 32;
+  const bool use_bits = kGrid && !korder && nkv <= C::kLiveWords * 32;
   if (use_bits) {
     const int nw = (nkv + 31) >> 5;
     for (int w = threadIdx.x; w < nw; w += kThreads) live_bits[w] = full_bits[w] = 0u;
@@ -145,8 +154,12 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
     }
     __syncthreads();
   }
-  auto next_live = [&](int j) -> int {
+  auto next_live = [&](int j) -> int {   // next visit index u >= j of a live tile
     if (!kGrid) return j;
+    if (korder) {
+      while (j < nu && !live(tile_at(j))) ++j;
+      return j;
+    }
     if (use_bits) {
       if (j >= nkv) return nkv;
       int w = j >> 5;
@@ -163,7 +176,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
     return j;
   };
   const int first = next_live(0);
-  const bool any = first < nkv;
+  const bool any = first < nu;
 
   if (warp == 8) {
     if (lane == 0) {
@@ -200,8 +213,8 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
           ptx::tma_load_4d(sQ + t * C::kTileBytes + x * C::kBoxBytes, &p.tm_q, q_full, x * 64, h,
                            (int)(row0 + t * BM), b);
       int it = 0;
-      for (int j = first; j < nkv; j = next_live(j + 1)) {
-        const int krow = (int)(hp.k_begin + (int64_t)j * BN);
+      for (int u = first; u < nu; u = next_live(u + 1)) {
+        const int krow = (int)(hp.k_begin + (int64_t)tile_at(u) * BN);
         for (int kv = 0; kv < 2; ++kv, ++it) {
           const int s = it % C::kStages;
           const uint32_t use = it / C::kStages;
@@ -262,11 +275,11 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
       qk(1, 0);
       commit(kv_empty + 0);
       // jj = index among the live KV tiles (stage / parity counter); j = tile index
-      for (int j = first, jj = 0; j < nkv; ++jj) {
+      for (int j = first, jj = 0; j < nu; ++jj) {
         const int jn = next_live(j + 1);
         const int itv = 2 * jj + 1, sv = itv % C::kStages;
         const int itk = 2 * jj + 2, sk = itk % C::kStages;
-        const bool more = jn < nkv;
+        const bool more = jn < nu;
         ptx::mbar_wait(kv_full + sv, (itv / C::kStages) & 1); FTRACE(0, jj);
         for (int c = 0; c < kPS; ++c) {
           ptx::mbar_wait(p_full + c, jj & 1); if (c == 0) FTRACE(1, jj);
@@ -314,10 +327,11 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
     const float c2 = p.scale_log2;
     float m_run = -INFINITY, l_run = 0.f;
 
-    for (int j = first, jj = 0; j < nkv; j = next_live(j + 1), ++jj) {
+    for (int u = first, jj = 0; u < nu; u = next_live(u + 1), ++jj) {
+      const int j = tile_at(u);
       const int64_t nvalid = lim - (int64_t)j * BN;
       uint64_t gk0 = 0, gk1 = 0;   // block-sparse grid: hidden key columns of this row
-      if (kGrid && !(use_bits && ((full_bits[j >> 5] >> (j & 31)) & 1u))) {
+      if (kGrid && hp.grid_skip && !(use_bits && ((full_bits[j >> 5] >> (j & 31)) & 1u))) {
         // (computed before the S wait so the table lookups overlap the MMA)
         const int nv = nvalid > BN ? BN : (nvalid < 0 ? 0 : (int)nvalid);
         const int64_t kt0 = hp.k_begin + (int64_t)j * BN;

@@ -175,6 +175,8 @@ def make_hop(plan: HopPlan, q: torch.Tensor, k: torch.Tensor, scale: float,
         h.flags = flags.data_ptr()
     if order is not None:
         h.dq_order = order.data_ptr()
+    if plan.key_order is not None:
+        h.key_order = plan.key_order.data_ptr()
     return h
 
 
@@ -217,6 +219,15 @@ class CudaKernels:
                   _ptr(st.o_acc), _ptr(st.m), _ptr(st.l), _ptr(o if finalize else None),
                   _ptr(lse if finalize else None), int(first), int(finalize),
                   _stream_handle(stream))
+
+    def fwd_init(self, state: FwdState, stream=None) -> None:
+        """Empty running state (PartialAttn.empty, local_attn.py:66-99): O_acc = 0,
+        m = -inf, l = 0, for a pass whose first computed hop covers only part of the
+        query block (start offset or a masked own block: Q_LATE_HALF comes first)."""
+        with torch.cuda.stream(stream) if stream is not None else _nullctx():
+            state.o_acc.zero_()
+            state.m.fill_(float("-inf"))
+            state.l.zero_()
 
     def fwd_finalize(self, state: FwdState, o, lse, stream=None) -> None:
         B, n, H, D = o.shape

@@ -568,41 +568,79 @@ def _recv_bufs(transport, likes, tag: int, spare, device=None):
     return list(spare)
 
 
-def _rotating(G: int):
-    """origin_fn of a pass whose payload rotates at slots h < G-1 (K/V, or Q/dO)."""
-    return lambda rank, h: (rank - h) % G if h < G - 1 else -1
+def _rotating(G: int, offset: int = 0):
+    """origin_fn of a pass whose payload rotates at slots h < G-1 (K/V, or Q/dO); slot
+    SHIFT (start offset) carries the sender's own block."""
+    return lambda rank, h: (rank if h == SHIFT else
+                            (rank - offset - h) % G if h < G - 1 else -1)
 
 
-def backward_slots(G: int) -> list:
-    """Exchange slots of a backward pass: K/V rotation at h < G-1, contribution
-    homecoming (one hop late) at h >= 2, and the final homecoming slot G."""
-    return [h for h in range(G) if h < G - 1 or h >= 2] + ([G] if G > 1 else [])
+def backward_slots(G: int, offset: int = 0) -> list:
+    """Exchange slots of a backward pass: the start-offset shift (SHIFT, only with an
+    offset), K/V rotation at h < G-1, contribution homecoming (one hop late) at h >= 2,
+    and the final homecoming slot G."""
+    return (([SHIFT] if offset and G > 1 else []) +
+            [h for h in range(G) if h < G - 1 or h >= _first_homecoming(offset)] +
+            ([G] if G > 1 else []))
+
+
+def _first_homecoming(offset: int) -> int:
+    """Slot of the first contribution homecoming: hop h's contribution goes home at
+    slot h + 1, except the own block's (hop 0 without a start offset)."""
+    return 1 if offset else 2
+
+
+SHIFT = -1      # exchange slot of the start-offset shift (before hop 0)
+
+
+def _shift(transport, S, payload, tag: int, offset: int, slog, recorder, kind: str):
+    """Start offset (initial_forward_body, ring.py:137-143; sim._initial_envelopes,
+    sim.py:406-419): before hop 0 rank r sends its own rotating payload to r + offset
+    and receives that of r - offset, so at hop h it holds block (r - offset - h) mod G.
+    Returns the received payload (engine- or transport-owned buffers)."""
+    G, r = transport.world, transport.rank
+    got = _recv_bufs(transport, payload, tag, None)
+    ops = ([(SEND, t, (r + offset) % G, tag) for t in payload] +
+           [(RECV, t, (r - offset) % G, tag) for t in got])
+    S.comm_after_compute()
+    if recorder is not None:
+        recorder.count_send(kind, ops)
+    transport.sendrecv(ops + slog.ops(SHIFT), S.comm)
+    S.compute_after_comm()
+    return got
 
 
 def ring_forward(q, k, v, scale: float, causal: bool, zigzag: bool, transport, kernels,
-                 n_valid: int | None = None, recorder=None, grid=None, check: str = "sync"):
+                 n_valid: int | None = None, recorder=None, grid=None, check: str = "sync",
+                 offset: int = 0):
     """One rank's forward pass.  Returns (O [B,n,H,D], lse [B,H,n] natural log).
     `n_valid`: real global length when the shards are zero-padded (reference pad=True).
     `recorder`: optional trace.PassRecorder (measured timeline + ledger, sim.py:118-261).
     `grid`: optional masks.GridMask bound to the global length (BlockGrid).
     `check`: when the pass's device error word is read ("sync" | "async" | "off",
-    kernels.finish; MaskError / NonFiniteError as in PartialAttn.finalize)."""
+    kernels.finish; MaskError / NonFiniteError as in PartialAttn.finalize).
+    `offset`: start offset (run_ring_pass(start_offset=...), sim.py:501-510): the merge
+    order rotates, values agree to rounding."""
     B, n, H, D = q.shape
     G, r = transport.world, transport.rank
+    offset %= G
     S = _Streams(q.device)
     o = torch.empty_like(q)
     lse = torch.empty(B, H, n, dtype=torch.float32, device=q.device)
     state = kernels.fwd_state(q, running=G > 1)
-    slog = SlotLog(transport, q.device, list(range(G - 1)), _rotating(G))
+    slog = SlotLog(transport, q.device, ([SHIFT] if offset else []) + list(range(G - 1)),
+                   _rotating(G, offset))
     if G > 1:
         transport.reserve({TAG_ROT: _nbytes(k, v), TAG_HDR: HDR_BYTES})
     cur_k, cur_v = k, v
+    if offset:
+        cur_k, cur_v = _shift(transport, S, (k, v), TAG_ROT, offset, slog, recorder, "forward")
     spare = None
     finalized = False
     computed = False             # a hop has merged into the running state
     prev = S.compute_mark()      # compute tail before hop h (buffers it still reads)
     for h in range(G):
-        plan = plan_hop(r, G, h, n, causal, zigzag, n_valid, grid)
+        plan = plan_hop(r, G, h, n, causal, zigzag, n_valid, grid, offset)
         exchanged = False
         # launch the hop's kernel first, then post the transfer on the comm stream:
         # both run concurrently (the comm waits only for the PREVIOUS hop's kernel,
@@ -611,7 +649,12 @@ def ring_forward(q, k, v, scale: float, causal: bool, zigzag: bool, transport, k
             recorder.mark(h, "compute_start", S.compute)
         if not plan.skip:
             fin = h == G - 1 and plan.covers_all_queries(n)
-            kernels.fwd(plan, q, cur_k, cur_v, scale, state, o, lse, first=not computed,
+            first = not computed
+            if first and not plan.covers_all_queries(n):
+                # the rows this rectangle leaves out need a defined (empty) state
+                kernels.fwd_init(state, stream=S.compute)
+                first = False
+            kernels.fwd(plan, q, cur_k, cur_v, scale, state, o, lse, first=first,
                         finalize=fin, stream=S.compute)
             finalized = finalized or fin
             computed = True
@@ -663,23 +706,24 @@ def split_own_hop(plan, n: int, world: int):
 
 
 def _part_exchange(r: int, G: int, n: int, causal: bool, zigzag: bool, hop: int, send_bufs,
-                   recv_bufs, n_valid=None, grid=None):
+                   recv_bufs, n_valid=None, grid=None, offset: int = 0):
     """Ops moving the dK/dV contribution computed at `hop` to its home rank, and
-    receiving into `recv_bufs` the one computed for ours.  Returns (ops, received?)."""
+    receiving into `recv_bufs` the one computed for ours (none when the hop's block is
+    the own block, which accumulates in place).  Returns (ops, received?)."""
     ops = []
-    mine = plan_hop(r, G, hop, n, causal, zigzag, n_valid, grid)
-    if not mine.skip:
+    mine = plan_hop(r, G, hop, n, causal, zigzag, n_valid, grid, offset)
+    if not mine.skip and mine.src != r:
         ops += [(SEND, send_bufs[0], mine.src, TAG_PART), (SEND, send_bufs[1], mine.src, TAG_PART)]
-    c = contributor_to(r, G, hop)
-    theirs = plan_hop(c, G, hop, n, causal, zigzag, n_valid, grid)
-    if not theirs.skip:
+    c = contributor_to(r, G, hop, offset)
+    got = c != r and not plan_hop(c, G, hop, n, causal, zigzag, n_valid, grid, offset).skip
+    if got:
         ops += [(RECV, recv_bufs[0], c, TAG_PART), (RECV, recv_bufs[1], c, TAG_PART)]
-    return ops, not theirs.skip
+    return ops, got
 
 
 def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: bool, transport,
                   kernels, n_valid: int | None = None, recorder=None, grid=None,
-                  check: str = "sync", deterministic: bool = False):
+                  check: str = "sync", deterministic: bool = False, offset: int = 0):
     """One rank's backward pass.  Returns (dq, dk, dv) in q's dtype.
 
     Contribution buffers are O(1) in the ring size: `own` accumulates this rank's
@@ -688,35 +732,53 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
     (burst_tl_accumulate) before the next hop -- the in-place accumulation of
     ring.backward_step (ring.py:239-241).  The own block is computed in two query
     halves (split_own_hop) so the final homecoming exchange overlaps a kernel.
-    `recorder`: optional trace.PassRecorder (see ring_forward)."""
+    `recorder`: optional trace.PassRecorder (see ring_forward).  `offset`: start
+    offset (K/V start shifted, see ring_forward); the own block then comes at hop
+    G - offset and is not split."""
     B, n, H, D = q.shape
     G, r = transport.world, transport.rank
+    offset %= G
     S = _Streams(q.device)
     st = kernels.bwd_prepare(o, dout, lse, stream=S.compute, deterministic=deterministic)
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     own = (kernels.part(k), kernels.part(v))
-    slog = SlotLog(transport, q.device, backward_slots(G), _rotating(G))
+    slog = SlotLog(transport, q.device, backward_slots(G, offset), _rotating(G, offset))
     if G > 1:
         transport.reserve({TAG_ROT: _nbytes(k, v), TAG_PART: _nbytes(*own), TAG_HDR: HDR_BYTES})
     send = [None, None]
     recv = None                  # contribution receive buffers (engine-owned or mailbox views)
     pending = False              # `recv` holds a contribution not yet folded into `own`
     own_last = None              # second query half of the own block (after hop G-1)
+    own_ready = False            # `own` holds a defined value
     cur_k, cur_v = k, v
+    if offset:
+        cur_k, cur_v = _shift(transport, S, (k, v), TAG_ROT, offset, slog, recorder, "backward")
     spare = None
+
+    def fold():
+        nonlocal own_ready
+        if own_ready:
+            kernels.accumulate(own, recv, k, stream=S.compute)
+        else:                    # (offset) a contribution landed before the own block ran
+            with torch.cuda.stream(S.compute) if S.cuda else _nullctx():
+                own[0].copy_(recv[0])
+                own[1].copy_(recv[1])
+            own_ready = True
+
     for h in range(G):
-        plan = plan_hop(r, G, h, n, causal, zigzag, n_valid, grid)
-        if h == 0:
+        plan = plan_hop(r, G, h, n, causal, zigzag, n_valid, grid, offset)
+        if h == 0 and not offset:
             plan, own_last = split_own_hop(plan, n, G)
         if recorder is not None:
             recorder.mark(h, "compute_start", S.compute)
         if pending:              # landed in the previous slot (compute waited for it)
-            kernels.accumulate(own, recv, k, stream=S.compute)
+            fold()
             pending = False
         # this slot's transfers wait for everything above: hop h-1's kernel (it made
         # the contribution sent now and last read `spare`) and the fold of `recv`
         ready = S.compute_mark()
-        if h == 0:
+        is_own = plan.src == r
+        if is_own:
             target = own
         else:
             if send[h % 2] is None:
@@ -724,9 +786,11 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
             target = send[h % 2]
         if not plan.skip:
             kernels.bwd(plan, q, cur_k, cur_v, dout, scale, st, target[0], target[1],
-                        accumulate=False, stream=S.compute)
-        elif h == 0:                  # own block fully masked (grid): no contribution
+                        accumulate=is_own and own_ready, stream=S.compute)
+            own_ready = own_ready or is_own
+        elif is_own and not own_ready:   # own block fully masked (grid): no contribution
             kernels.zero_(target, stream=S.compute)
+            own_ready = True
         if recorder is not None:
             recorder.mark(h, "compute_end", S.compute)
         ops = []
@@ -734,16 +798,16 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
             spare = _recv_bufs(transport, (k, v), TAG_ROT, spare)
             ops += [(SEND, cur_k, (r + 1) % G, TAG_ROT), (SEND, cur_v, (r + 1) % G, TAG_ROT),
                     (RECV, spare[0], (r - 1) % G, TAG_ROT), (RECV, spare[1], (r - 1) % G, TAG_ROT)]
-        if h >= 2:
+        if h >= _first_homecoming(offset):
             recv = _recv_bufs(transport, own, TAG_PART, recv)
             p_ops, got = _part_exchange(r, G, n, causal, zigzag, h - 1, send[(h - 1) % 2],
-                                        recv, n_valid, grid)
+                                        recv, n_valid, grid, offset)
             ops += p_ops
             pending = got
         # every rank takes part in every exchange slot (a slot depends only on
         # h and G), even with no op of its own: keeps loopback/collective
         # transports in lockstep when causal hops are skipped
-        slot = h < G - 1 or h >= 2
+        slot = h < G - 1 or h >= _first_homecoming(offset)
         if slot:
             S.comm_wait(ready)
             if recorder is not None:
@@ -764,11 +828,11 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
         if recorder is not None:
             recorder.mark(G, "compute_start", S.compute)
         if pending:
-            kernels.accumulate(own, recv, k, stream=S.compute)
+            fold()
         ready = S.compute_mark()
         recv = _recv_bufs(transport, own, TAG_PART, recv)
         p_ops, got = _part_exchange(r, G, n, causal, zigzag, G - 1, send[(G - 1) % 2], recv,
-                                    n_valid, grid)
+                                    n_valid, grid, offset)
         S.comm_wait(ready)
         if recorder is not None:
             recorder.count_send("backward", p_ops)
@@ -794,16 +858,16 @@ def ring_backward(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: boo
 
 
 def _qpart_exchange(r: int, G: int, n: int, causal: bool, zigzag: bool, hop: int, send_buf,
-                    recv_buf, n_valid=None, grid=None):
+                    recv_buf, n_valid=None, grid=None, offset: int = 0):
     """Ops moving the dQ contribution computed at `hop` (for the visiting query
     block) to that block's home rank, and receiving into `recv_buf` the one
-    computed for ours.  Returns (ops, received?)."""
+    computed for ours (none for the own block).  Returns (ops, received?)."""
     ops = []
-    src = (r - hop) % G                        # origin of the query block I processed
-    if not plan_hop(src, G, (src - r) % G, n, causal, zigzag, n_valid, grid).skip:
+    src = (r - offset - hop) % G               # origin of the query block I processed
+    if src != r and not plan_hop(src, G, (src - r) % G, n, causal, zigzag, n_valid, grid).skip:
         ops.append((SEND, send_buf, src, TAG_PART))
-    c = (r + hop) % G                          # the rank that processed MY block at `hop`
-    got = not plan_hop(r, G, (r - c) % G, n, causal, zigzag, n_valid, grid).skip
+    c = (r + offset + hop) % G                 # the rank that processed MY block at `hop`
+    got = c != r and not plan_hop(r, G, (r - c) % G, n, causal, zigzag, n_valid, grid).skip
     if got:
         ops.append((RECV, recv_buf, c, TAG_PART))
     return ops, got
@@ -811,7 +875,8 @@ def _qpart_exchange(r: int, G: int, n: int, causal: bool, zigzag: bool, hop: int
 
 def ring_backward_qtravel(q, k, v, o, lse, dout, scale: float, causal: bool, zigzag: bool,
                           transport, kernels, n_valid: int | None = None, recorder=None,
-                          grid=None, check: str = "sync", deterministic: bool = False):
+                          grid=None, check: str = "sync", deterministic: bool = False,
+                          offset: int = 0):
     """One rank's backward pass with the REFERENCE's payload:
     the query-side record (Q, dO, lse/D statistics) travels the ring and K/V/dK/dV
     stay pinned (BackwardBody ring.py:65-83, backward_step ring.py:221-242,
@@ -822,19 +887,24 @@ def ring_backward_qtravel(q, k, v, o, lse, dout, scale: float, causal: bool, zig
     lands (O(1) buffers).  The own block runs in two query halves like
     ring_backward, the second one overlapping the last dQ homecoming.  Wire bytes
     per hop: 2·n·H·D·elem (Q, dO) + statistics + an fp32 dQ contribution, vs K/V +
-    fp32 dK/dV for ring_backward.  Returns (dq, dk, dv) in q's dtype."""
+    fp32 dK/dV for ring_backward.  `offset`: start offset (the query record of rank
+    r - offset starts on rank r, sim._initial_envelopes sim.py:406-419).  Returns
+    (dq, dk, dv) in q's dtype."""
     B, n, H, D = q.shape
     G, r = transport.world, transport.rank
+    offset %= G
     S = _Streams(q.device)
     st = kernels.bwd_prepare(o, dout, lse, stream=S.compute, deterministic=deterministic)
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     dk_acc, dv_acc = kernels.part(k), kernels.part(v)
     payload = [q, dout] + kernels.stats_tensors(st)      # the visiting query block
-    slog = SlotLog(transport, q.device, backward_slots(G), _rotating(G))
+    slog = SlotLog(transport, q.device, backward_slots(G, offset), _rotating(G, offset))
     if G > 1:
         dq_like = kernels.dq_like(q)         # shape/dtype of a dQ contribution (meta)
         transport.reserve({TAG_ROT: _nbytes(*payload), TAG_PART: _nbytes(dq_like),
                            TAG_HDR: HDR_BYTES})
+    if offset:
+        payload = _shift(transport, S, payload, TAG_ROT, offset, slog, recorder, "backward")
     spare = None
     send = [None, None]
     recv = None                  # dQ contribution receive buffer (engine-owned or a mailbox view)
@@ -842,9 +912,9 @@ def ring_backward_qtravel(q, k, v, o, lse, dout, scale: float, causal: bool, zig
     own_last = None
     first_kv = True
     for h in range(G):
-        src = (r - h) % G
+        src = (r - offset - h) % G
         plan = plan_hop(src, G, (src - r) % G, n, causal, zigzag, n_valid, grid)
-        if h == 0:
+        if h == 0 and not offset:
             plan, own_last = split_own_hop(plan, n, G)
         if recorder is not None:
             recorder.mark(h, "compute_start", S.compute)
@@ -852,7 +922,7 @@ def ring_backward_qtravel(q, k, v, o, lse, dout, scale: float, causal: bool, zig
             kernels.accumulate_dq(st, recv, q, stream=S.compute)
             pending = False
         ready = S.compute_mark()
-        if h == 0:
+        if src == r:
             vst = st                                     # own queries: own dQ accumulator
         else:
             # zeroed on the compute stream: the buffer was last read by slot h-1's
@@ -870,14 +940,14 @@ def ring_backward_qtravel(q, k, v, o, lse, dout, scale: float, causal: bool, zig
             spare = _recv_bufs(transport, payload, TAG_ROT, spare)
             ops += [(SEND, t, (r + 1) % G, TAG_ROT) for t in payload]
             ops += [(RECV, t, (r - 1) % G, TAG_ROT) for t in spare]
-        if h >= 2:
+        if h >= _first_homecoming(offset):
             recv = _recv_bufs(transport, (dq_like,), TAG_PART,
                               None if recv is None else (recv,), q.device)[0]
             p_ops, got = _qpart_exchange(r, G, n, causal, zigzag, h - 1, send[(h - 1) % 2],
-                                         recv, n_valid, grid)
+                                         recv, n_valid, grid, offset)
             ops += p_ops
             pending = got
-        slot = h < G - 1 or h >= 2
+        slot = h < G - 1 or h >= _first_homecoming(offset)
         if slot:
             S.comm_wait(ready)
             if recorder is not None:
@@ -902,7 +972,7 @@ def ring_backward_qtravel(q, k, v, o, lse, dout, scale: float, causal: bool, zig
         recv = _recv_bufs(transport, (dq_like,), TAG_PART,
                           None if recv is None else (recv,), q.device)[0]
         p_ops, got = _qpart_exchange(r, G, n, causal, zigzag, G - 1, send[(G - 1) % 2], recv,
-                                     n_valid, grid)
+                                     n_valid, grid, offset)
         S.comm_wait(ready)
         if recorder is not None:
             recorder.count_send("backward", p_ops)

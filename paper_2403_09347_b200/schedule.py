@@ -51,6 +51,7 @@ class HopPlan:
     q_map: PosMap
     k_map: PosMap
     grid: object = None  # masks.GridMask (bound) applied element-wise, or None
+    key_order: object = None  # device int32 key-tile permutation (LAO forward), or None
 
     @property
     def skip(self) -> bool:
@@ -70,9 +71,11 @@ def shard_map(rank: int, world: int, n_local: int, zigzag: bool) -> PosMap:
     return PosMap(rank * n_local, rank * n_local + n_local, n_local)
 
 
-def source_rank(rank: int, world: int, hop: int) -> int:
-    """Origin of the K/V block a rank holds at `hop` (sim.py:565, ring.py:143)."""
-    return (rank - hop) % world
+def source_rank(rank: int, world: int, hop: int, offset: int = 0) -> int:
+    """Origin of the K/V block a rank holds at `hop` (sim.py:565, ring.py:143); a
+    start offset rotates the initial assignment (initial_forward_body, ring.py:137-143:
+    device i starts with block (i - offset) mod G)."""
+    return (rank - offset - hop) % world
 
 
 def valid_rows(rank: int, world: int, n_local: int, zigzag: bool, n_valid: int | None) -> int:
@@ -90,12 +93,12 @@ def valid_rows(rank: int, world: int, n_local: int, zigzag: bool, n_valid: int |
 
 
 def plan_hop(rank: int, world: int, hop: int, n_local: int, causal: bool,
-             zigzag: bool, n_valid: int | None = None, grid=None) -> HopPlan:
+             zigzag: bool, n_valid: int | None = None, grid=None, offset: int = 0) -> HopPlan:
     """Rectangle of one hop, with an optional block-sparse grid (masks.GridMask,
     bound to the global length): a rectangle whose every (query cell, key cell)
     pair is skipped becomes SKIP (BlockMask.decision, masking.py:79-106), any
     other keeps the grid for element-level masking in the kernels."""
-    plan = _plan_hop(rank, world, hop, n_local, causal, zigzag, n_valid)
+    plan = _plan_hop(rank, world, hop, n_local, causal, zigzag, n_valid, offset)
     if grid is None or plan.skip:
         return plan
     qp = plan.q_map.positions(plan.q_begin + plan.q_len)[plan.q_begin:]
@@ -111,18 +114,18 @@ def plan_hop(rank: int, world: int, hop: int, n_local: int, causal: bool,
 
 
 def _plan_hop(rank: int, world: int, hop: int, n_local: int, causal: bool,
-              zigzag: bool, n_valid: int | None = None) -> HopPlan:
+              zigzag: bool, n_valid: int | None = None, offset: int = 0) -> HopPlan:
     """Rectangle of one hop.  With padding (n_valid = real global length), padded
     keys are excluded by shortening the key range (BlockMask.with_padding,
     masking.py:74-75); under the causal rule they are invisible to every real
     query anyway, since they sit after all real positions."""
-    src = source_rank(rank, world, hop)
+    src = source_rank(rank, world, hop, offset)
     qm = shard_map(rank, world, n_local, zigzag)
     km = shard_map(src, world, n_local, zigzag)
     n = n_local
     if not causal:
         kv = valid_rows(src, world, n_local, zigzag, n_valid)
-        if kv == 0 and hop > 0:
+        if kv == 0 and src != rank:
             return HopPlan(hop, rank, src, SKIP, 0, 0, 0, 0, False, qm, km)
         return HopPlan(hop, rank, src, FULL, 0, n, 0, kv, False, qm, km)
     if src == rank:
@@ -137,14 +140,14 @@ def _plan_hop(rank: int, world: int, hop: int, n_local: int, causal: bool,
     return HopPlan(hop, rank, src, SKIP, 0, 0, 0, 0, False, qm, km)
 
 
-def owner_of_contribution(rank: int, world: int, hop: int) -> int:
+def owner_of_contribution(rank: int, world: int, hop: int, offset: int = 0) -> int:
     """dK/dV computed at `hop` belong to the visiting block's home rank."""
-    return source_rank(rank, world, hop)
+    return source_rank(rank, world, hop, offset)
 
 
-def contributor_to(rank: int, world: int, hop: int) -> int:
+def contributor_to(rank: int, world: int, hop: int, offset: int = 0) -> int:
     """Rank that computed, at `hop`, a contribution for `rank`'s own block."""
-    return (rank + hop) % world
+    return (rank + offset + hop) % world
 
 
 def hop_flops(plan: HopPlan, batch: int, heads: int, d: int) -> tuple[float, float]:

@@ -96,6 +96,24 @@ def lao_case(name, rows, cols, dim, row_offset, col_offset, n_total, causal, see
     print("wrote", name)
 
 
+def order_case(name, rows, cols, dim, row_offset, col_offset, n_total, causal, seed, order):
+    """local_forward_tiled with a permuted key-tile order (key_tile_order,
+    local_attn.py:212-225), 128x128 tiles (the GPU kernels' tile)."""
+    rng = np.random.Generator(np.random.Philox(seed))
+    q, k, v = (rng.standard_normal((r, dim)) for r in (rows, cols, cols))
+    mask = BlockMask(causal=True) if causal else None
+    part = local_forward_tiled(Matrix.from_array(q), Matrix.from_array(k),
+                               Matrix.from_array(v), dim ** -0.5, TileSpec(128, 128), mask,
+                               row_offset=row_offset, col_offset=col_offset,
+                               n_total=n_total, key_tile_order=list(order))
+    o, lse = part.finalize()
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), q=q, k=k, v=v,
+                        o=o.array, lse=lse.array, order=np.array(order),
+                        meta=np.array([rows, cols, dim, row_offset, col_offset, n_total,
+                                       int(causal), seed]))
+    print("wrote", name)
+
+
 def grid_cases():
     """Block-sparse grid masks through the whole ring (mask_from_spec dict form,
     masking.py:150-180), with and without the causal constraint."""
@@ -114,6 +132,10 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "grid":
         grid_cases()
         sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "order":
+        order_case("lao_order_r256_c640_d64_causal", 256, 640, 64, 512, 0, 768, True, 21,
+                   [3, 0, 4, 2, 1])
+        sys.exit(0)
     # BASELINE.json configs[0]: seq 1024, d 64, 2 heads, G 2, fp32, non-causal.
     # 128x128 tiles (the default SRAM tile gives identical math, 100x slower).
     ring_case("c1_seq1024_d64_h2_g2_f32", 1024, 64, 2, 2, "single", tile=128)
@@ -131,3 +153,5 @@ if __name__ == "__main__":
     lao_case("lao_r12_c20_d8_causal", 12, 20, 8, 16, 4, 40, True, 7)
     lao_case("lao_r16_c16_d8_full", 16, 16, 8, 0, 16, 32, False, 8)
     grid_cases()
+    order_case("lao_order_r256_c640_d64_causal", 256, 640, 64, 512, 0, 768, True, 21,
+               [3, 0, 4, 2, 1])

@@ -33,9 +33,15 @@ class OracleKernels:
         self.launches = 0
 
     def fwd_state(self, q, running=True):
+        # undefined until a first hop writes it, like the CUDA state (torch.empty)
         B, n, H, D = q.shape
-        return {"o": np.zeros((B, H, n, D)), "m": np.full((B, H, n), -np.inf),
-                "l": np.zeros((B, H, n))}
+        return {"o": np.full((B, H, n, D), np.nan), "m": np.full((B, H, n), np.nan),
+                "l": np.full((B, H, n), np.nan)}
+
+    def fwd_init(self, state, stream=None):
+        state["o"][:] = 0.0
+        state["m"][:] = -np.inf
+        state["l"][:] = 0.0
 
     def finish(self, state, check, stream=None, where="BurstAttention"):
         """The oracle raises its errors synchronously (MaskError / NonFiniteError)."""

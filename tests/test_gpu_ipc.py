@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _worker(rank, world, port, causal, zigzag, payload, out_dir):
+def _worker(rank, world, port, causal, zigzag, payload, out_dir, offset=0):
     import torch.distributed as dist
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -34,7 +34,7 @@ def _worker(rank, world, port, causal, zigzag, payload, out_dir):
         for t in sh[:3]:
             t.grad = None
         o, lse = burst_attn_func(sh[0], sh[1], sh[2], causal=causal, zigzag=zigzag,
-                                 bwd_payload=payload, _transport=tr)
+                                 bwd_payload=payload, start_offset=offset, _transport=tr)
         o.backward(sh[3])
     torch.cuda.synchronize()
     hu = sorted(tr.host_us)
@@ -48,9 +48,12 @@ def _worker(rank, world, port, causal, zigzag, payload, out_dir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("causal,zigzag,payload", [(False, False, "kv"), (True, True, "kv"),
-                                                   (True, True, "q")])
-def test_ipc_transport_two_processes_one_gpu(causal, zigzag, payload, tmp_path):
+@pytest.mark.parametrize("causal,zigzag,payload,offset", [(False, False, "kv", 0),
+                                                          (True, True, "kv", 0),
+                                                          (True, True, "q", 0),
+                                                          (True, True, "kv", 1),
+                                                          (False, False, "q", 1)])
+def test_ipc_transport_two_processes_one_gpu(causal, zigzag, payload, offset, tmp_path):
     import torch.multiprocessing as mp
     from gpu_utils import make_inputs, max_abs, oracle_ring
     from paper_2403_09347_b200.schedule import unshard
@@ -59,7 +62,7 @@ def test_ipc_transport_two_processes_one_gpu(causal, zigzag, payload, tmp_path):
     port = s.getsockname()[1]
     s.close()
     world = 2
-    mp.start_processes(_worker, args=(world, port, causal, zigzag, payload, str(tmp_path)),
+    mp.start_processes(_worker, args=(world, port, causal, zigzag, payload, str(tmp_path), offset),
                        nprocs=world, start_method="spawn", join=True)
     parts = [torch.load(tmp_path / f"r{r}.pt") for r in range(world)]
     q, k, v, do = make_inputs(1, 1024, 2, 128, seed=42)

@@ -342,3 +342,27 @@ def test_unaligned_query_tile_ignores_stats_past_the_end():
         assert torch.isfinite(dk[0, :, h]).all()
         assert max_abs(dk[0, :, h], ref_dk.numpy()) < BF16_TOL
         assert max_abs(dv[0, :, h], ref_dv.numpy()) < BF16_TOL
+
+
+@pytest.mark.parametrize("world,causal,zigzag,payload,offset", [(4, True, True, "kv", 1),
+                                                                (4, True, True, "q", 3),
+                                                                (3, False, False, "kv", 2),
+                                                                (4, True, False, "q", 2)])
+def test_ring_start_offset(world, causal, zigzag, payload, offset):
+    """start_offset rotates the initial K/V (or query-record) assignment (ring.py:137-143,
+    sim.py:406-419): one extra exchange, then the same values as offset 0 to rounding."""
+    from paper_2403_09347_b200 import run_ring_pass
+    N = 256 * world * (2 if zigzag else 1)
+    q, k, v, do = make_inputs(1, N, 2, 128, seed=offset + world)
+    poison_allocator()
+    res = run_ring_pass(q, k, v, world, causal=causal, dout=do, zigzag=zigzag,
+                        bwd_payload=payload, start_offset=offset)
+    base = run_ring_pass(q, k, v, world, causal=causal, dout=do, zigzag=zigzag,
+                         bwd_payload=payload)
+    torch.cuda.synchronize()
+    o, lse, dq, dk, dv = oracle_ring(q, k, v, do, world, causal, zigzag)
+    assert max_abs(res.out, o) < BF16_TOL
+    assert max_abs(res.lse, lse) < 1e-2
+    for name, got, ref in (("dq", res.dq, dq), ("dk", res.dk, dk), ("dv", res.dv, dv)):
+        assert max_abs(got, ref) < BF16_TOL, name
+        assert max_abs(got, getattr(base, name).float().cpu().numpy()) < 1e-2, name

@@ -117,3 +117,35 @@ def test_bf16_round():
     assert r[0] == 1.0 and r[1] == 1.0  # ties to even
     assert r[2] == np.float32(1.0 + 2 ** -7)
     assert abs(r[3] - x[3]) <= abs(x[3]) * 2 ** -8
+
+
+def test_key_tile_order_matches_reference_golden(golden):
+    """local_forward_tiled with a permuted key_tile_order (local_attn.py:212-225),
+    causal in global coordinates, 128x128 tiles, against the reference's output."""
+    g = golden("lao_order_r256_c640_d64_causal")
+    rows, cols, dim, r0, c0, n_total, causal, seed = (int(x) for x in g["meta"])
+    qp, kp = np.arange(r0, r0 + rows), np.arange(c0, c0 + cols)
+    part = orc.local_forward_tiled(g["q"], g["k"], g["v"], dim ** -0.5, 128, 128, qp, kp,
+                                   bool(causal), key_tile_order=list(g["order"]))
+    o, lse = part.finalize()
+    assert np.max(np.abs(o - g["o"])) < 1e-12
+    assert np.max(np.abs(lse - g["lse"])) < 1e-12
+    # the order is value-irrelevant to rounding (pkg/tests/test_local_attn.py:145-155)
+    o2, lse2 = orc.local_forward_tiled(g["q"], g["k"], g["v"], dim ** -0.5, 128, 128, qp, kp,
+                                       bool(causal)).finalize()
+    assert np.max(np.abs(o2 - o)) < 1e-13 and np.max(np.abs(lse2 - lse)) < 1e-13
+    with pytest.raises(ValueError):
+        orc.local_forward_tiled(g["q"], g["k"], g["v"], 0.1, 128, 128, qp, kp, True,
+                                key_tile_order=[0, 0, 1, 2, 3])
+
+
+def test_lao_key_tile_order_must_be_permutation():
+    """The product's LAO entry validates the order before touching the device
+    (ShapeError, local_attn.py:223-225)."""
+    import torch
+    from paper_2403_09347_b200 import ShapeError, local_forward
+    x = torch.zeros(1, 256, 1, 64)
+    with pytest.raises(ShapeError):
+        local_forward(x, x, x, key_tile_order=[0, 0])
+    with pytest.raises(ShapeError):
+        local_forward(x, x, x, key_tile_order=[0, 1, 2])
