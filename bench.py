@@ -386,13 +386,17 @@ def run_ours(args, cfg, rank, world, local_rank):
         step(q, k, v, do, recs)
         torch.cuda.synchronize()
         sf, sb = comm_summary(recs[0].events()), comm_summary(recs[1].events())
-        vals = torch.tensor([sf["send_us"], sf["hidden_us"], sb["send_us"], sb["hidden_us"]],
+        vals = torch.tensor([sf["send_us"], sf["hidden_us"], sb["send_us"], sb["hidden_us"],
+                             sf["exposed_us"], sb["exposed_us"]],
                             device=cdev, dtype=torch.float64)
         allv = [torch.zeros_like(vals) for _ in range(world)]
         dist.all_gather(allv, vals)
         tot = torch.stack(allv).sum(0).tolist()
         comm_trace = {"fwd_send_us_all_ranks": tot[0], "fwd_hidden_frac": tot[1] / max(tot[0], 1e-9),
                       "bwd_send_us_all_ranks": tot[2], "bwd_hidden_frac": tot[3] / max(tot[2], 1e-9),
+                      "fwd_exposed_us_all_ranks": tot[4], "bwd_exposed_us_all_ranks": tot[5],
+                      "fwd_stall_hidden_frac": max(0.0, 1 - tot[4] / max(tot[0], 1e-9)),
+                      "bwd_stall_hidden_frac": max(0.0, 1 - tot[5] / max(tot[2], 1e-9)),
                       "fwd_bytes_per_rank": recs[0].ledger.bytes_sent_forward,
                       "bwd_bytes_per_rank": recs[1].ledger.bytes_sent_backward,
                       "fwd_GBps_per_rank": recs[0].ledger.bytes_sent_forward

@@ -177,12 +177,24 @@ def measure_overlap(events) -> dict:
 
 def comm_summary(events) -> dict:
     """Comm-stream busy time and the share of it hidden under compute, over all
-    rounds and devices (north star: >= 90 % of ring communication hidden)."""
+    rounds and devices (north star: >= 90 % of ring communication hidden).
+
+    hidden_frac: the reference's interval overlap (sim.py:238-261) -- the part of
+    each send interval covered by the same rank's compute interval of that round.
+    stall_hidden_frac: 1 - exposed / send time, where `exposed` is how long the
+    compute stream had to wait for an exchange after its kernel of the round had
+    finished (recv_ready - compute_end, when positive).  The two agree when every
+    rank owns a GPU; when the ranks of a loopback ring share ONE GPU their kernels
+    queue behind each other, so a transfer often runs before its own rank's kernel
+    has started (not "covered", yet nobody waits for it) -- only the stall measure
+    says whether communication cost time there."""
     spans: dict[tuple[int, int], dict[str, float]] = {}
     for e in events:
         spans.setdefault((e["round"], e["device"]), {})[e["kind"]] = e["t_virtual"]
-    send_us = hidden_us = 0.0
+    send_us = hidden_us = exposed_us = compute_us = 0.0
     for kinds in spans.values():
+        if "compute_start" in kinds and "compute_end" in kinds:
+            compute_us += kinds["compute_end"] - kinds["compute_start"]
         if "send_start" not in kinds:
             continue
         dur = kinds["send_end"] - kinds["send_start"]
@@ -191,8 +203,14 @@ def comm_summary(events) -> dict:
             lo = max(kinds["compute_start"], kinds["send_start"])
             hi = min(kinds["compute_end"], kinds["send_end"])
             hidden_us += max(0.0, hi - lo)
+            ready = kinds.get("recv_ready", kinds["send_end"])
+            exposed_us += max(0.0, ready - kinds["compute_end"])
+        else:
+            exposed_us += dur
     return {"send_us": send_us, "hidden_us": hidden_us,
-            "hidden_frac": hidden_us / send_us if send_us > 0 else None}
+            "hidden_frac": hidden_us / send_us if send_us > 0 else None,
+            "exposed_us": exposed_us, "compute_us": compute_us,
+            "stall_hidden_frac": max(0.0, 1.0 - exposed_us / send_us) if send_us > 0 else None}
 
 
 @dataclass
