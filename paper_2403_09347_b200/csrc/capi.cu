@@ -161,6 +161,11 @@ int set_smem(K kernel, int bytes) {
 int* flags_of(const burst_hop* h) { return h->flags ? h->flags : device_flags(); }
 int* flags_or_default(int32_t* f) { return f ? f : device_flags(); }
 
+// Default backward: key-tile pairs in 2-CTA clusters sharing Q/dO (lao_bwd4 kPair).
+#ifndef BURST_BWD_PAIRS
+#define BURST_BWD_PAIRS 1
+#endif
+
 int grid_for(int64_t work, int block) {
   int64_t g = (work + block - 1) / block;
   if (g > 148 * 32) g = 148 * 32;
@@ -240,8 +245,31 @@ int launch_bwd4_bf16(const burst_hop* h, const void* q, const void* k, const voi
     kernel<<<grid, bwd4::kThreads, bwd4::Cfg<D>::kSmemBytes, st>>>(p);
     return BURST_OK;
   };
+  // key-tile pairs as 2-CTA clusters sharing Q/dO loads (TMA multicast); an odd tile
+  // count gets one key-less CTA that only consumes its half of the shared stages
+  auto go_pair = [&](auto kernel) -> int {
+    if (int e = set_smem(kernel, bwd4::Cfg<D>::kSmemBytes)) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((grid.x + 1) & ~1u, grid.y, grid.z);
+    cfg.blockDim = dim3(bwd4::kThreads);
+    cfg.dynamicSmemBytes = bwd4::Cfg<D>::kSmemBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, p));
+    return BURST_OK;
+  };
+  constexpr bool kPairs = (D == 128) && BURST_BWD_PAIRS;
   if (h->dq_order)
     rc = h->grid_skip ? go(bwd4::lao_bwd4_kernel<D, true, true>) : go(bwd4::lao_bwd4_kernel<D, false, true>);
+  else if constexpr (kPairs)
+    rc = h->grid_skip ? go_pair(bwd4::lao_bwd4_kernel<D, true, false, kPairs>)
+                      : go_pair(bwd4::lao_bwd4_kernel<D, false, false, kPairs>);
   else
     rc = h->grid_skip ? go(bwd4::lao_bwd4_kernel<D, true, false>) : go(bwd4::lao_bwd4_kernel<D, false, false>);
   if (rc) return rc;

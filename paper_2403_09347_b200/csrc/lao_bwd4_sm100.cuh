@@ -107,9 +107,15 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 // the instantiation without it keeps the dense loops free of the skip bookkeeping.
 // kOrdered: deterministic dQ (p.dq_order set); its own instantiation keeps the turn
 // bookkeeping out of the drain's register budget in the default kernel.
-template <int D, bool kGrid, bool kOrdered>
+// kPair: launched as 2-CTA clusters over key tiles (2p, 2p+1) that walk the SAME query
+// tiles; each CTA TMA-loads one 64-column box of every Q and dO tile and multicasts it
+// to both (half the L2 reads of Q/dO, which are ~40% of the backward's L2 traffic); a
+// stage is refilled only once both CTAs have released it (2-count empty barriers fed
+// by multicast MMA commits).
+template <int D, bool kGrid, bool kOrdered, bool kPair = false>
 __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_constant__ Params p) {
   using C = Cfg<D>;
+  static_assert(!kPair || D == 128, "the paired backward splits Q/dO tiles by 64-column box");
   // SW128 tiles need 1024-byte alignment; the declaration asks the compiler for it and
   // the runtime check below can then only fail on a toolchain that ignores it, in
   // which case the launch reports a CudaError (flag bit 2) instead of trapping.
@@ -154,6 +160,10 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
   const int64_t bh = (int64_t)b * hp.heads + h;
   const int64_t k0 = hp.k_begin + (int64_t)blockIdx.x * BN;   // first key row of this CTA
   const int64_t k_end = hp.k_begin + hp.k_len;
+  // the key rows whose query walk this CTA follows: its own, or its cluster pair's 256
+  const uint32_t crank = kPair ? ptx::cluster_rank() : 0u;
+  const int64_t kw0 = kPair ? hp.k_begin + (int64_t)(blockIdx.x & ~1u) * BN : k0;
+  const int64_t kwrows = (kw0 + (kPair ? 2 : 1) * BN < k_end ? kw0 + (kPair ? 2 : 1) * BN : k_end) - kw0;
   const int64_t q_end = hp.q_begin + hp.q_len;
   const int64_t NTq = ceil_div(hp.n_q, 128);
   const int64_t NTk = ceil_div(hp.n_k, 128);
@@ -164,7 +174,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
   // frontier are masked like causal columns.
   int64_t qlo = hp.q_begin;
   if (hp.causal) {
-    const int64_t first_q = count_le(hp.q_map, hp.n_q, pos_of(hp.k_map, k0) - 1);
+    const int64_t first_q = count_le(hp.q_map, hp.n_q, pos_of(hp.k_map, kw0) - 1);
     if (first_q > qlo) qlo = first_q;
   }
   const int64_t qs = (qlo / BM) * BM;
@@ -174,16 +184,16 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
   // profiles/r01_rotation_exp.txt).  Deterministic mode walks the tiles in order
   // (key tile j follows j - 1 through every tile).
   constexpr bool ordered = kOrdered;
-  const int rot = (nq > 0 && !ordered) ? (int)((blockIdx.x * 7u) % (unsigned)nq) : 0;
+  const unsigned walker = kPair ? blockIdx.x >> 1 : blockIdx.x;
+  const int rot = (nq > 0 && !ordered) ? (int)((walker * 7u) % (unsigned)nq) : 0;
   auto qtile = [&](int i) -> int64_t { int j = i + rot; if (j >= nq) j -= nq; return qs + (int64_t)j * BM; };
   // Block-sparse grid: query tiles whose every (query, key) pair with this CTA's keys
   // lies in skipped cells are skipped by every role.  Roles count LIVE tiles (stages,
   // barrier parities); the producer, P/dS and drain map them back to tile indices.
-  const int64_t krows = (k0 + BN < k_end ? k0 + BN : k_end) - k0;
-  auto live = [&](int i) -> bool {
+  auto live = [&](int i) -> bool {   // (kPair: live for either CTA of the pair)
     if (!kGrid) return true;
     const int64_t q0 = qtile(i) < hp.q_begin ? hp.q_begin : qtile(i);
-    return grid_rect_live(hp, q0, (qtile(i) + BM < q_end ? qtile(i) + BM : q_end) - q0, k0, krows);
+    return grid_rect_live(hp, q0, (qtile(i) + BM < q_end ? qtile(i) + BM : q_end) - q0, kw0, kwrows);
   };
   // The predicate is evaluated once per tile by the whole CTA into a SMEM bitmap (up to
   // kLiveWords * 32 tiles); every role then finds the next live tile with __ffs.
@@ -213,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
       ptx::mbar_init(kv_full, 1);
       for (int s = 0; s < 2; ++s) {
         ptx::mbar_init(qdo_full + s, 1);
-        ptx::mbar_init(qdo_empty + s, 1);
+        ptx::mbar_init(qdo_empty + s, kPair ? 2 : 1);
       }
       ptx::mbar_init(s_full, 1);
       ptx::mbar_init(p_full, 2 * BN);
@@ -224,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
       ptx::mbar_init(dkv_full, 1);
       ptx::mbar_init(dp_full, 1);
       ptx::mbar_init(do_full, 1);
-      ptx::mbar_init(do_empty, 1);
+      ptx::mbar_init(do_empty, kPair ? 2 : 1);
       ptx::fence_mbar_init();
       ptx::tma_prefetch_desc(&p.tm_q);
       ptx::tma_prefetch_desc(&p.tm_k);
@@ -249,7 +259,10 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
     if (lane == 0 && mine) atomicAdd(tmem_holder + 1, (uint32_t)mine);
   }
   ptx::tc_fence_before();
-  __syncthreads();
+  if (kPair)
+    ptx::cluster_sync();   // both CTAs' barriers exist before either multicasts into them
+  else
+    __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tbase = *tmem_holder;
   if (kGrid) nlive = (int)tmem_holder[1];
@@ -280,9 +293,13 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
         const int64_t q0 = qtile(ti);
         ptx::mbar_wait(qdo_empty + s, ((j >> 1) & 1) ^ 1);
         ptx::mbar_expect_tx(qdo_full + s, C::kTileBytes + C::kStatBytes);
-        for (int x = 0; x < C::kBoxes; ++x)
-          ptx::tma_load_4d(sQ + s * C::kTileBytes + x * C::kBoxBytes, &p.tm_q, qdo_full + s,
-                           x * 64, h, (int)q0, b);
+        if (kPair)
+          ptx::tma_load_4d_mc(sQ + s * C::kTileBytes + crank * C::kBoxBytes, &p.tm_q, qdo_full + s,
+                              (int)crank * 64, h, (int)q0, b, 3);
+        else
+          for (int x = 0; x < C::kBoxes; ++x)
+            ptx::tma_load_4d(sQ + s * C::kTileBytes + x * C::kBoxBytes, &p.tm_q, qdo_full + s,
+                             x * 64, h, (int)q0, b);
         const float* st = p.stats + bh * NTq * 128 + q0;
         bulk_load(sStat + s * 2 * BM, st, BM * 4, qdo_full + s);
         bulk_load(sStat + s * 2 * BM + BM, st + (int64_t)hp.batch * hp.heads * NTq * 128, BM * 4,
@@ -291,8 +308,12 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
       auto load_do = [&](int j, int ti) {
         ptx::mbar_wait(do_empty, (j & 1) ^ 1);
         ptx::mbar_expect_tx(do_full, C::kTileBytes);
-        for (int x = 0; x < C::kBoxes; ++x)
-          ptx::tma_load_4d(sdO + x * C::kBoxBytes, &p.tm_do, do_full, x * 64, h, (int)qtile(ti), b);
+        if (kPair)
+          ptx::tma_load_4d_mc(sdO + crank * C::kBoxBytes, &p.tm_do, do_full, (int)crank * 64, h,
+                              (int)qtile(ti), b, 3);
+        else
+          for (int x = 0; x < C::kBoxes; ++x)
+            ptx::tma_load_4d(sdO + x * C::kBoxBytes, &p.tm_do, do_full, x * 64, h, (int)qtile(ti), b);
       };
       int tq = next_live(0), td = tq;      // next tile of the Q and of the dO load stream
       load_q(0, tq); tq = next_live(tq + 1);
@@ -356,7 +377,10 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
                         id_mnmn, kk > 0);
           ptx::mma_commit(dq_full);
           ptx::mma_commit(ds_empty);
-          ptx::mma_commit(qdo_empty + (i & 1));
+          if (kPair)
+            ptx::mma_commit_mc(qdo_empty + (i & 1), 3);   // this CTA released the stage, in both
+          else
+            ptx::mma_commit(qdo_empty + (i & 1));
         }
         __syncwarp();
       };
@@ -378,7 +402,10 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
           for (int kk = 0; kk < BM / 16; ++kk)
             ptx::mma_ts(tbase + kDV, tbase + kS + (kk < 4 ? kk * 8 : 32 + kk * 8),
                         dOm + (uint64_t)(kk * 2048 >> 4), id_kmn, (i > 0 || kk > 0) ? 1u : 0u);
-          ptx::mma_commit(do_empty);
+          if (kPair)
+            ptx::mma_commit_mc(do_empty, 3);
+          else
+            ptx::mma_commit(do_empty);
         }
         __syncwarp();
         bool st_done = !more, dkq_done = false;
@@ -641,7 +668,10 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
 
   __syncwarp();
   ptx::tc_fence_before();
-  __syncthreads();
+  if (kPair)
+    ptx::cluster_sync();   // no multicast load or remote arrive may target an exited CTA
+  else
+    __syncthreads();
   if (warp == 12) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tbase, 512);
