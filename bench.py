@@ -507,7 +507,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     roof = None
     if bwd_ms:
         ach = bwd_fl / (bwd_ms / 1e3) / 1e12
-        roof = {"bound": "tensor", "kernel": "lao_bwd4_kernel<128> (LAO backward, sm_100a tcgen05, 2 P/dS warpgroups, TMA bulk dQ reduction)",
+        roof = {"bound": "tensor", "kernel": "lao_bwd4_kernel<128> (LAO backward, sm_100a tcgen05, key-tile pairs in 2-CTA clusters sharing Q/dO by TMA multicast, 2 P/dS warpgroups, TMA bulk dQ reduction)",
                 "achieved": ach, "peak": peak_sus, "unit": "TFLOP/s", "frac": ach / peak_sus,
                 "peak_kind": f"bf16 sustained ({peak_src}); kernel runs inside a long step",
                 "frac_of_burst_peak": ach / peak_burst, "traffic": traffic,
