@@ -166,6 +166,29 @@ int* flags_or_default(int32_t* f) { return f ? f : device_flags(); }
 #define BURST_BWD_PAIRS 1
 #endif
 
+#ifndef BURST_FWD_PAIRS
+#define BURST_FWD_PAIRS 1
+#endif
+
+// Launch `kernel` as 2-CTA clusters along x (grid.x rounded up to even).
+template <typename K, typename P>
+int launch_pair(K kernel, dim3 grid, int threads, int smem, cudaStream_t st, const P& p) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((grid.x + 1) & ~1u, grid.y, grid.z);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, p));
+  return BURST_OK;
+}
+
 int grid_for(int64_t work, int block) {
   int64_t g = (work + block - 1) / block;
   if (g > 148 * 32) g = 148 * 32;
@@ -189,13 +212,21 @@ int launch_fwd_bf16(const burst_hop* h, const void* q, const void* k, const void
 #ifdef BURST_TRACE
   p.trace = trace_buffer();
 #endif
-  if ((rc = set_smem(fwd::lao_fwd_kernel<D, false>, fwd::Cfg<D>::kSmemBytes))) return rc;
-  if ((rc = set_smem(fwd::lao_fwd_kernel<D, true>, fwd::Cfg<D>::kSmemBytes))) return rc;
   dim3 grid((unsigned)ceil_div(h->q_len, 2 * fwd::BM), h->heads, h->batch);
-  if (h->grid_skip || h->key_order)
-    fwd::lao_fwd_kernel<D, true><<<grid, fwd::kThreads, fwd::Cfg<D>::kSmemBytes, st>>>(p);
-  else
-    fwd::lao_fwd_kernel<D, false><<<grid, fwd::kThreads, fwd::Cfg<D>::kSmemBytes, st>>>(p);
+  const bool general = h->grid_skip || h->key_order;
+  constexpr bool kPairs = (D == 128) && BURST_FWD_PAIRS;
+  if constexpr (kPairs) {
+    // query-block pairs as 2-CTA clusters sharing K/V (TMA multicast); an odd block count
+    // gets one row-less CTA that only consumes its half of the shared stages
+    auto kernel = general ? fwd::lao_fwd_kernel<D, true, true> : fwd::lao_fwd_kernel<D, false, true>;
+    if ((rc = set_smem(kernel, fwd::Cfg<D>::kSmemBytes))) return rc;
+    rc = launch_pair(kernel, grid, fwd::kThreads, fwd::Cfg<D>::kSmemBytes, st, p);
+    if (rc) return rc;
+  } else {
+    auto kernel = general ? fwd::lao_fwd_kernel<D, true> : fwd::lao_fwd_kernel<D, false>;
+    if ((rc = set_smem(kernel, fwd::Cfg<D>::kSmemBytes))) return rc;
+    kernel<<<grid, fwd::kThreads, fwd::Cfg<D>::kSmemBytes, st>>>(p);
+  }
   CHECK_LAUNCH();
   return BURST_OK;
 }
@@ -249,20 +280,7 @@ int launch_bwd4_bf16(const burst_hop* h, const void* q, const void* k, const voi
   // count gets one key-less CTA that only consumes its half of the shared stages
   auto go_pair = [&](auto kernel) -> int {
     if (int e = set_smem(kernel, bwd4::Cfg<D>::kSmemBytes)) return e;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((grid.x + 1) & ~1u, grid.y, grid.z);
-    cfg.blockDim = dim3(bwd4::kThreads);
-    cfg.dynamicSmemBytes = bwd4::Cfg<D>::kSmemBytes;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, p));
-    return BURST_OK;
+    return launch_pair(kernel, grid, bwd4::kThreads, bwd4::Cfg<D>::kSmemBytes, st, p);
   };
   constexpr bool kPairs = (D == 128) && BURST_BWD_PAIRS;
   if (h->dq_order)

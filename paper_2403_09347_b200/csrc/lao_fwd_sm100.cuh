@@ -82,9 +82,14 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
 // local_forward_tiled's key_tile_order, local_attn.py:212-225); the dense instantiation
 // keeps its loops free of that bookkeeping.  Roles walk "visit" indices u; tile j =
 // key_order[u] (or u).
-template <int D, bool kGrid>
+// kPair: launched as 2-CTA clusters over adjacent query blocks that walk the SAME key
+// tiles; each CTA TMA-loads one 64-column box of every K and V tile with
+// .multicast::cluster into both (half the L2 reads of K/V); a stage is refilled once
+// both CTAs released it (2-count empty barriers fed by multicast tcgen05.commit).
+template <int D, bool kGrid, bool kPair = false>
 __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_constant__ Params p) {
   using C = Cfg<D>;
+  static_assert(!kPair || D == 128, "the paired forward splits K/V tiles by 64-column box");
   // FMA-pipe exp2 share (profiles/r01_poly_exp2.txt): 5/16 measured best for dense hops,
   // 3/8 for the grid-masked instantiation (c3_sparse: 122.5 vs 126.3 ms per launch)
   constexpr int kPolyMod = kGrid ? 8 : BURST_POLY_MOD;
@@ -111,11 +116,16 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
   // order shortens the tail wave of the grid)
   const int64_t xb = hp.causal ? (int64_t)(gridDim.x - 1 - blockIdx.x) : (int64_t)blockIdx.x;
   const int64_t row0 = hp.q_begin + xb * (2 * BM);
+  // the query rows whose key walk this CTA follows: its own 256, or its pair's 512
+  const uint32_t crank = kPair ? ptx::cluster_rank() : 0u;
+  const int64_t xb_peer = hp.causal ? (int64_t)(gridDim.x - 1 - (blockIdx.x ^ 1u)) : (int64_t)(blockIdx.x ^ 1u);
+  const int64_t wrow0 = kPair ? hp.q_begin + (xb < xb_peer ? xb : xb_peer) * (2 * BM) : row0;
+  const int64_t wrow1 = wrow0 + (kPair ? 4 : 2) * BM;   // exclusive
 
   // Key span this CTA needs: causal => a prefix of the hop's keys (monotone maps).
   int64_t kspan = hp.k_len;
   if (hp.causal) {
-    int64_t last = (row0 + 2 * BM < q_end ? row0 + 2 * BM : q_end) - 1;
+    int64_t last = (wrow1 < q_end ? wrow1 : q_end) - 1;
     int64_t cnt = count_le(hp.k_map, hp.n_k, pos_of(hp.q_map, last)) - hp.k_begin;
     kspan = cnt < kspan ? cnt : kspan;
     if (kspan < 0) kspan = 0;
@@ -129,11 +139,12 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
   // Block-sparse grid: KV tiles whose every (query, key) pair lies in skipped cells
   // are skipped by every role (each evaluates the same predicate).
   const int64_t qrows = (row0 + 2 * BM < q_end ? row0 + 2 * BM : q_end) - row0;
-  auto live = [&](int j) -> bool {
+  const int64_t wrows = (wrow1 < q_end ? wrow1 : q_end) - wrow0;
+  auto live = [&](int j) -> bool {   // (kPair: live for either CTA of the pair)
     if (!kGrid) return true;
     if (j >= nkv) return false;
     const int64_t kr = kspan - (int64_t)j * BN;
-    return grid_rect_live(hp, row0, qrows, hp.k_begin + (int64_t)j * BN, kr < BN ? kr : BN);
+    return grid_rect_live(hp, wrow0, wrows, hp.k_begin + (int64_t)j * BN, kr < BN ? kr : BN);
   };
   // The predicate is evaluated once per tile by the whole CTA into a SMEM bitmap (up to
   // kLiveWords * 32 tiles); every role then finds the next live tile with __ffs.  A
@@ -183,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
       ptx::mbar_init(q_full, 1);
       for (int s = 0; s < C::kStages; ++s) {
         ptx::mbar_init(kv_full + s, 1);
-        ptx::mbar_init(kv_empty + s, 1);
+        ptx::mbar_init(kv_empty + s, kPair ? 2 : 1);
       }
       for (int t = 0; t < 2; ++t) {
         ptx::mbar_init(s_full + t, 1);
@@ -199,7 +210,10 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
     ptx::tmem_alloc(tmem_holder, 512);
   }
   ptx::tc_fence_before();
-  __syncthreads();
+  if (kPair)
+    ptx::cluster_sync();   // both CTAs' barriers exist before either multicasts into them
+  else
+    __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tbase = *tmem_holder;
   if (warp >= 8) {
@@ -221,9 +235,13 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
           ptx::mbar_wait(kv_empty + s, (use & 1) ^ 1);
           ptx::mbar_expect_tx(kv_full + s, C::kTileBytes);
           const CUtensorMap* tm = kv == 0 ? &p.tm_k : &p.tm_v;
-          for (int x = 0; x < C::kBoxes; ++x)
-            ptx::tma_load_4d(sKV + s * C::kTileBytes + x * C::kBoxBytes, tm, kv_full + s, x * 64,
-                             h, krow, b);
+          if (kPair)
+            ptx::tma_load_4d_mc(sKV + s * C::kTileBytes + crank * C::kBoxBytes, tm, kv_full + s,
+                                (int)crank * 64, h, krow, b, 3);
+          else
+            for (int x = 0; x < C::kBoxes; ++x)
+              ptx::tma_load_4d(sKV + s * C::kTileBytes + x * C::kBoxBytes, tm, kv_full + s, x * 64,
+                               h, krow, b);
         }
       }
     }
@@ -268,12 +286,21 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
         if (ptx::elect_one()) ptx::mma_commit(b);
         __syncwarp();
       };
+      auto release = [&](uint64_t* b) {   // a K/V stage: this CTA is done with it (in both)
+        if (ptx::elect_one()) {
+          if (kPair)
+            ptx::mma_commit_mc(b, 3);
+          else
+            ptx::mma_commit(b);
+        }
+        __syncwarp();
+      };
       ptx::mbar_wait(q_full, 0);
       ptx::mbar_wait(kv_full + 0, 0);
       ptx::tc_fence_after();
       qk(0, 0);
       qk(1, 0);
-      commit(kv_empty + 0);
+      release(kv_empty + 0);
       // jj = index among the live KV tiles (stage / parity counter); j = tile index
       for (int j = first, jj = 0; j < nu; ++jj) {
         const int jn = next_live(j + 1);
@@ -296,10 +323,10 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
           ptx::tc_fence_after();
           pv(1, sv, jj > 0, c);
         }
-        commit(kv_empty + sv);
+        release(kv_empty + sv);
         if (more) {
           qk(1, sk);
-          commit(kv_empty + sk);
+          release(kv_empty + sk);
         }
         j = jn;
       }
@@ -513,7 +540,10 @@ __global__ void __launch_bounds__(kThreads, 1) lao_fwd_kernel(const __grid_const
 
   __syncwarp();
   ptx::tc_fence_before();
-  __syncthreads();
+  if (kPair)
+    ptx::cluster_sync();   // no multicast load or remote arrive may target an exited CTA
+  else
+    __syncthreads();
   if (warp == 8) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tbase, 512);
