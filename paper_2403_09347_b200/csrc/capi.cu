@@ -161,26 +161,28 @@ int set_smem(K kernel, int bytes) {
 int* flags_of(const burst_hop* h) { return h->flags ? h->flags : device_flags(); }
 int* flags_or_default(int32_t* f) { return f ? f : device_flags(); }
 
-// Default backward: key-tile pairs in 2-CTA clusters sharing Q/dO (lao_bwd4 kPair).
-#ifndef BURST_BWD_PAIRS
-#define BURST_BWD_PAIRS 1
+// Default backward: consecutive key tiles in clusters of this many CTAs sharing Q/dO
+// loads (lao_bwd4 kCl; 1 = no clusters).
+#ifndef BURST_BWD_CLUSTER
+#define BURST_BWD_CLUSTER 2
 #endif
 
 #ifndef BURST_FWD_PAIRS
 #define BURST_FWD_PAIRS 1
 #endif
 
-// Launch `kernel` as 2-CTA clusters along x (grid.x rounded up to even).
+// Launch `kernel` as `cl`-CTA clusters along x (grid.x rounded up to a multiple of cl).
 template <typename K, typename P>
-int launch_pair(K kernel, dim3 grid, int threads, int smem, cudaStream_t st, const P& p) {
+int launch_pair(K kernel, dim3 grid, int threads, int smem, cudaStream_t st, const P& p,
+                int cl = 2) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((grid.x + 1) & ~1u, grid.y, grid.z);
+  cfg.gridDim = dim3((grid.x + cl - 1) / cl * cl, grid.y, grid.z);
   cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.x = cl;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -280,14 +282,19 @@ int launch_bwd4_bf16(const burst_hop* h, const void* q, const void* k, const voi
   // count gets one key-less CTA that only consumes its half of the shared stages
   auto go_pair = [&](auto kernel) -> int {
     if (int e = set_smem(kernel, bwd4::Cfg<D>::kSmemBytes)) return e;
-    return launch_pair(kernel, grid, bwd4::kThreads, bwd4::Cfg<D>::kSmemBytes, st, p);
+    return launch_pair(kernel, grid, bwd4::kThreads, bwd4::Cfg<D>::kSmemBytes, st, p,
+                       D == 128 ? BURST_BWD_CLUSTER : 1);
   };
-  constexpr bool kPairs = (D == 128) && BURST_BWD_PAIRS;
+  constexpr int kCl = D == 128 ? BURST_BWD_CLUSTER : 1;
+  if (kCl == 4) {
+    if ((rc = make_tmap(&p.tm_q64, q, h->n_q, h->heads, D, h->batch, 64))) return rc;
+    if ((rc = make_tmap(&p.tm_do64, dout, h->n_q, h->heads, D, h->batch, 64))) return rc;
+  }
   if (h->dq_order)
     rc = h->grid_skip ? go(bwd4::lao_bwd4_kernel<D, true, true>) : go(bwd4::lao_bwd4_kernel<D, false, true>);
-  else if constexpr (kPairs)
-    rc = h->grid_skip ? go_pair(bwd4::lao_bwd4_kernel<D, true, false, kPairs>)
-                      : go_pair(bwd4::lao_bwd4_kernel<D, false, false, kPairs>);
+  else if constexpr (kCl > 1)
+    rc = h->grid_skip ? go_pair(bwd4::lao_bwd4_kernel<D, true, false, kCl>)
+                      : go_pair(bwd4::lao_bwd4_kernel<D, false, false, kCl>);
   else
     rc = h->grid_skip ? go(bwd4::lao_bwd4_kernel<D, true, false>) : go(bwd4::lao_bwd4_kernel<D, false, false>);
   if (rc) return rc;

@@ -59,6 +59,7 @@ struct Cfg {
 
 struct Params {
   CUtensorMap tm_q, tm_k, tm_v, tm_do;
+  CUtensorMap tm_q64, tm_do64;   // 64-row boxes (clusters of 4)
   const float* stats;    // [2][B*H][NTq*128]: lse*log2e, D
   float* dq_acc;         // TL over n_q
   float* dk_acc;         // TL over n_k
@@ -107,15 +108,19 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 // the instantiation without it keeps the dense loops free of the skip bookkeeping.
 // kOrdered: deterministic dQ (p.dq_order set); its own instantiation keeps the turn
 // bookkeeping out of the drain's register budget in the default kernel.
-// kPair: launched as 2-CTA clusters over key tiles (2p, 2p+1) that walk the SAME query
-// tiles; each CTA TMA-loads one 64-column box of every Q and dO tile and multicasts it
-// to both (half the L2 reads of Q/dO, which are ~40% of the backward's L2 traffic); a
-// stage is refilled only once both CTAs have released it (2-count empty barriers fed
+// kCl (cluster size 1, 2 or 4): launched as kCl-CTA clusters over consecutive key tiles
+// that walk the SAME query tiles; each CTA TMA-loads 1/kCl of every Q and dO tile (a
+// 64-column box, or a 64-row half of one for kCl = 4) and multicasts it to all (1/kCl
+// of the L2 reads of Q/dO, which are ~40% of the unclustered backward's L2 traffic); a
+// stage is refilled only once every CTA has released it (kCl-count empty barriers fed
 // by multicast MMA commits).
-template <int D, bool kGrid, bool kOrdered, bool kPair = false>
+template <int D, bool kGrid, bool kOrdered, int kCl = 1>
 __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_constant__ Params p) {
   using C = Cfg<D>;
-  static_assert(!kPair || D == 128, "the paired backward splits Q/dO tiles by 64-column box");
+  static_assert(kCl == 1 || D == 128, "clustered backward splits Q/dO tiles by 64-column box");
+  static_assert(kCl == 1 || kCl == 2 || kCl == 4, "cluster of 1, 2 or 4 CTAs");
+  constexpr bool kPair = kCl > 1;
+  constexpr uint16_t kMask = (uint16_t)((1u << kCl) - 1u);
   // SW128 tiles need 1024-byte alignment; the declaration asks the compiler for it and
   // the runtime check below can then only fail on a toolchain that ignores it, in
   // which case the launch reports a CudaError (flag bit 2) instead of trapping.
@@ -162,8 +167,8 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
   const int64_t k_end = hp.k_begin + hp.k_len;
   // the key rows whose query walk this CTA follows: its own, or its cluster pair's 256
   const uint32_t crank = kPair ? ptx::cluster_rank() : 0u;
-  const int64_t kw0 = kPair ? hp.k_begin + (int64_t)(blockIdx.x & ~1u) * BN : k0;
-  const int64_t kwrows = (kw0 + (kPair ? 2 : 1) * BN < k_end ? kw0 + (kPair ? 2 : 1) * BN : k_end) - kw0;
+  const int64_t kw0 = hp.k_begin + (int64_t)(blockIdx.x & ~(unsigned)(kCl - 1)) * BN;
+  const int64_t kwrows = (kw0 + kCl * BN < k_end ? kw0 + kCl * BN : k_end) - kw0;
   const int64_t q_end = hp.q_begin + hp.q_len;
   const int64_t NTq = ceil_div(hp.n_q, 128);
   const int64_t NTk = ceil_div(hp.n_k, 128);
@@ -184,7 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
   // profiles/r01_rotation_exp.txt).  Deterministic mode walks the tiles in order
   // (key tile j follows j - 1 through every tile).
   constexpr bool ordered = kOrdered;
-  const unsigned walker = kPair ? blockIdx.x >> 1 : blockIdx.x;
+  const unsigned walker = blockIdx.x / kCl;
   const int rot = (nq > 0 && !ordered) ? (int)((walker * 7u) % (unsigned)nq) : 0;
   auto qtile = [&](int i) -> int64_t { int j = i + rot; if (j >= nq) j -= nq; return qs + (int64_t)j * BM; };
   // Block-sparse grid: query tiles whose every (query, key) pair with this CTA's keys
@@ -223,7 +228,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
       ptx::mbar_init(kv_full, 1);
       for (int s = 0; s < 2; ++s) {
         ptx::mbar_init(qdo_full + s, 1);
-        ptx::mbar_init(qdo_empty + s, kPair ? 2 : 1);
+        ptx::mbar_init(qdo_empty + s, kCl);
       }
       ptx::mbar_init(s_full, 1);
       ptx::mbar_init(p_full, 2 * BN);
@@ -234,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
       ptx::mbar_init(dkv_full, 1);
       ptx::mbar_init(dp_full, 1);
       ptx::mbar_init(do_full, 1);
-      ptx::mbar_init(do_empty, kPair ? 2 : 1);
+      ptx::mbar_init(do_empty, kCl);
       ptx::fence_mbar_init();
       ptx::tma_prefetch_desc(&p.tm_q);
       ptx::tma_prefetch_desc(&p.tm_k);
@@ -293,9 +298,13 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
         const int64_t q0 = qtile(ti);
         ptx::mbar_wait(qdo_empty + s, ((j >> 1) & 1) ^ 1);
         ptx::mbar_expect_tx(qdo_full + s, C::kTileBytes + C::kStatBytes);
-        if (kPair)
+        if (kCl == 2)
           ptx::tma_load_4d_mc(sQ + s * C::kTileBytes + crank * C::kBoxBytes, &p.tm_q, qdo_full + s,
-                              (int)crank * 64, h, (int)q0, b, 3);
+                              (int)crank * 64, h, (int)q0, b, kMask);
+        else if (kCl == 4)   // 64-row half (crank >> 1) of column box (crank & 1)
+          ptx::tma_load_4d_mc(sQ + s * C::kTileBytes + (crank & 1) * C::kBoxBytes + (crank >> 1) * 8192,
+                              &p.tm_q64, qdo_full + s, (int)(crank & 1) * 64, h,
+                              (int)(q0 + (crank >> 1) * 64), b, kMask);
         else
           for (int x = 0; x < C::kBoxes; ++x)
             ptx::tma_load_4d(sQ + s * C::kTileBytes + x * C::kBoxBytes, &p.tm_q, qdo_full + s,
@@ -308,9 +317,13 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
       auto load_do = [&](int j, int ti) {
         ptx::mbar_wait(do_empty, (j & 1) ^ 1);
         ptx::mbar_expect_tx(do_full, C::kTileBytes);
-        if (kPair)
+        if (kCl == 2)
           ptx::tma_load_4d_mc(sdO + crank * C::kBoxBytes, &p.tm_do, do_full, (int)crank * 64, h,
-                              (int)qtile(ti), b, 3);
+                              (int)qtile(ti), b, kMask);
+        else if (kCl == 4)
+          ptx::tma_load_4d_mc(sdO + (crank & 1) * C::kBoxBytes + (crank >> 1) * 8192, &p.tm_do64,
+                              do_full, (int)(crank & 1) * 64, h, (int)(qtile(ti) + (crank >> 1) * 64),
+                              b, kMask);
         else
           for (int x = 0; x < C::kBoxes; ++x)
             ptx::tma_load_4d(sdO + x * C::kBoxBytes, &p.tm_do, do_full, x * 64, h, (int)qtile(ti), b);
@@ -378,7 +391,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
           ptx::mma_commit(dq_full);
           ptx::mma_commit(ds_empty);
           if (kPair)
-            ptx::mma_commit_mc(qdo_empty + (i & 1), 3);   // this CTA released the stage, in both
+            ptx::mma_commit_mc(qdo_empty + (i & 1), kMask);   // this CTA released the stage, in all
           else
             ptx::mma_commit(qdo_empty + (i & 1));
         }
@@ -403,7 +416,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
             ptx::mma_ts(tbase + kDV, tbase + kS + (kk < 4 ? kk * 8 : 32 + kk * 8),
                         dOm + (uint64_t)(kk * 2048 >> 4), id_kmn, (i > 0 || kk > 0) ? 1u : 0u);
           if (kPair)
-            ptx::mma_commit_mc(do_empty, 3);
+            ptx::mma_commit_mc(do_empty, kMask);
           else
             ptx::mma_commit(do_empty);
         }
