@@ -35,6 +35,10 @@
 namespace burst {
 namespace bwd4 {
 
+#ifndef BURST_BWD_ROT   // query-tile rotation multiplier per walker (CTA or cluster)
+#define BURST_BWD_ROT 7
+#endif
+
 constexpr int BM = 128;  // query rows per iteration
 constexpr int BN = 128;  // key rows per CTA
 constexpr int kThreads = 512;
@@ -190,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
   // (key tile j follows j - 1 through every tile).
   constexpr bool ordered = kOrdered;
   const unsigned walker = blockIdx.x / kCl;
-  const int rot = (nq > 0 && !ordered) ? (int)((walker * 7u) % (unsigned)nq) : 0;
+  const int rot = (nq > 0 && !ordered) ? (int)((walker * (unsigned)BURST_BWD_ROT) % (unsigned)nq) : 0;
   auto qtile = [&](int i) -> int64_t { int j = i + rot; if (j >= nq) j -= nq; return qs + (int64_t)j * BM; };
   // Block-sparse grid: query tiles whose every (query, key) pair with this CTA's keys
   // lies in skipped cells are skipped by every role.  Roles count LIVE tiles (stages,
