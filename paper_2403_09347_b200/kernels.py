@@ -67,7 +67,6 @@ def check_qkv(q, k, v) -> tuple[int, int, int, int]:
     return B, n, H, D
 
 
-STATS_SLACK = 128   # floats of readable slack after the backward stats (burst_bwd_preprocess)
 
 
 def ws_floats(B: int, H: int, D: int, n: int) -> int:
@@ -86,7 +85,7 @@ class FwdState:
 
 @dataclass
 class BwdState:
-    stats: torch.Tensor   # flat [2][B*H][ceil(n/128)*128] (lse*log2e, D) + STATS_SLACK
+    stats: torch.Tensor   # flat [2][B*H][ceil(n/128)*128] (lse*log2e, D)
     dq_acc: torch.Tensor  # TL fp32
     flags: torch.Tensor   # [1] int32 error word of the pass
     order: torch.Tensor | None = None   # deterministic mode: burst_hop.dq_order words
@@ -259,12 +258,9 @@ class CudaKernels:
         nt = -(-n // 128) * 128
         with torch.cuda.stream(stream) if stream is not None else _nullctx():
             flags = self._flags(o.device)
-        # [2][B*H][nt] + STATS_SLACK zeroed floats: a query tile that starts off the
-        # 128-row grid (unaligned zigzag chunks) bulk-loads up to 127 values past the
-        # last row, which must stay inside the allocation (include/burst_b200.h)
-        stats = torch.empty(2 * B * H * nt + STATS_SLACK, dtype=torch.float32, device=o.device)
-        with torch.cuda.stream(stream) if stream is not None else _nullctx():
-            stats[2 * B * H * nt:].zero_()
+        # [2][B*H][nt]: the backward loads whole 128-row tiles of the block (padded rows
+        # are written by burst_bwd_preprocess), never past the last tile
+        stats = torch.empty(2 * B * H * nt, dtype=torch.float32, device=o.device)
         order = (torch.empty(B * H * (-(-n // 128)), dtype=torch.int32, device=o.device)
                  if deterministic else None)
         st = BwdState(stats,
