@@ -25,8 +25,9 @@
 //   warps 8-11  dQ drain (thread = query row of the dQ tile)
 //   warp  12    TMA producer (+ TMEM allocator);  warp 13 tcgen05.mma issuer
 // TMEM (512 cols for D=128): S^T [0,128) with P^T (bf16) of query half h written
-// over S^T columns [64h, 64h+32) by the warpgroup that read them; dP^T [128,256)
-// (then dQ_i once dS_i is built); dV [256,256+D); dK [256+D,256+2D).
+// over S^T columns [64h, 64h+32) by the warpgroup that read them; dP^T [128,256), with
+// dS^T (bf16, the A operand of dK) written the same way over [128+64h, +32), then dQ_i
+// once dK_i has read it; dV [256,256+D); dK [256+D,256+2D).
 #pragma once
 #include <cuda.h>
 #include "common.cuh"
@@ -358,7 +359,6 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
       const uint64_t dOk = ptx::make_sdesc(ptx::smem_u32(sdO), 0, 1024);           // K-major (dP^T)
       const uint64_t dOm = ptx::make_sdesc(ptx::smem_u32(sdO), C::kBoxBytes, 1024); // MN-major (dV)
       const uint64_t dQm0 = ptx::make_sdesc(ptx::smem_u32(sQ), C::kBoxBytes, 1024); // MN-major (dK)
-      const uint64_t dSk = ptx::make_sdesc(ptx::smem_u32(sdS), 0, 1024);           // dS^T K-major (dK)
       const uint64_t dSm = ptx::make_sdesc(ptx::smem_u32(sdS), 16384, 1024);       // dS MN-major (dQ)
       const uint64_t dKm = ptx::make_sdesc(ptx::smem_u32(sK), C::kBoxBytes, 1024);  // K MN-major (dQ)
       constexpr uint64_t kStage = (uint64_t)(C::kTileBytes >> 4);
@@ -386,7 +386,9 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
           const uint64_t qm = dQm0 + (i & 1) * kStage;
 #pragma unroll
           for (int kk = 0; kk < BM / 16; ++kk)
-            ptx::mma_ss(tbase + kDK, dSk + (uint64_t)(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4),
+            // A = dS^T from TMEM; the dQ MMAs below overwrite those columns, and in-order
+            // execution of one thread's MMAs keeps that after this read
+            ptx::mma_ts(tbase + kDK, tbase + kDP + (kk < 4 ? kk * 8 : 32 + kk * 8),
                         qm + (uint64_t)(kk * 2048 >> 4), id_kmn, (i > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
           for (int kk = 0; kk < BN / 16; ++kk)
@@ -559,8 +561,12 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
           *reinterpret_cast<uint4*>(rowp + ((ch ^ (t & 7)) << 4)) =
               make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
         }
+        // dS^T (bf16) also over the dP^T columns this warpgroup has read, in the P^T
+        // layout: the A operand of dK from TMEM (32 KB less SMEM read per step)
+        ptx::tmem_st16(tbase + lane_off + kDP + 64 * hq + 16 * qc, pk);
       }
       if (hq == 0) BTRACE4(21, i);
+      ptx::tmem_wait_st();
       ptx::fence_proxy_async_smem();
       ptx::tc_fence_before();
       ptx::mbar_arrive(ds_full); if (hq == 0) BTRACE4(6, i); else BTRACE4(23, i);
