@@ -63,6 +63,10 @@ def test_ring_bf16_loopback(world, causal, zigzag):
     (2, 3, 1536, 128, 2, True, True),     # batch x heads > 1 through a zigzag ring
     (3, 2, 1024, 64, 4, False, False),    # head_dim 64 bf16 ring
     (2, 1, 2304, 128, 2, False, False),   # shard of 1152 rows: partial last query/key tiles
+    (2, 3, 2304, 128, 3, True, True),     # odd ring (G=3), zigzag chunks of 384 rows, 3 key tiles
+    (1, 2, 1920, 128, 1, True, False),    # 15 key tiles / 7.5 query blocks: a key-less CTA in the
+                                          # last backward pair, a row-less CTA in the last forward pair
+    (2, 2, 3840, 128, 5, False, False),   # G=5, 768-row shards: odd cluster counts per hop
 ])
 def test_ring_bf16_batched(B, H, N, D, world, causal, zigzag):
     """Batch and head indexing of every kernel (TMA coordinates, TL workspaces, stats)
