@@ -55,7 +55,7 @@ struct Cfg {
   static constexpr int kPayload = 2 * kTileBytes + 2 * kTileBytes + kTileBytes + kDsBytes +
                                   2 * kQuarterBytes + 2 * kStatBytes;
   static constexpr int kLiveWords = 64;    // live-query-tile bitmap (grid masks): 2048 tiles
-  static constexpr int kBarBytes = 128 + 4 * kLiveWords;
+  static constexpr int kBarBytes = 136 + 4 * kLiveWords;
   static constexpr int kMaxSmem = 232448;
   static constexpr int kSmemBytes =
       (kPayload + kBarBytes + 1024 <= kMaxSmem) ? kPayload + kBarBytes + 1024 : kMaxSmem;
@@ -161,7 +161,8 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
   uint64_t* dp_full = bars + 12;
   uint64_t* do_full = bars + 13;
   uint64_t* do_empty = bars + 14;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 15);
+  uint64_t* dst_full = bars + 15;   // dS^T in TMEM (dK may start; dS still on its way to SMEM)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 16);
 
   const burst_hop& hp = p.hop;
   const int warp = threadIdx.x >> 5;
@@ -238,6 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
       ptx::mbar_init(s_full, 1);
       ptx::mbar_init(p_full, 2 * BN);
       ptx::mbar_init(ds_full, 2 * BN);
+      ptx::mbar_init(dst_full, 2 * BN);
       ptx::mbar_init(ds_empty, 1);
       ptx::mbar_init(dq_full, 1);
       ptx::mbar_init(dq_empty, BM);
@@ -381,7 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
         }
         __syncwarp();
       };
-      auto dkq_mma = [&](int i) {   // dK += dS^T Q ; dQ_i = dS K (into the drained dP^T columns)
+      auto dk_mma = [&](int i) {   // dK += dS^T Q (A = dS^T in TMEM); last reader of Q_i
         if (ptx::elect_one()) {
           const uint64_t qm = dQm0 + (i & 1) * kStage;
 #pragma unroll
@@ -390,16 +392,21 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
             // execution of one thread's MMAs keeps that after this read
             ptx::mma_ts(tbase + kDK, tbase + kDP + (kk < 4 ? kk * 8 : 32 + kk * 8),
                         qm + (uint64_t)(kk * 2048 >> 4), id_kmn, (i > 0 || kk > 0) ? 1u : 0u);
+          if (kPair)
+            ptx::mma_commit_mc(qdo_empty + (i & 1), kMask);   // this CTA released the stage, in all
+          else
+            ptx::mma_commit(qdo_empty + (i & 1));
+        }
+        __syncwarp();
+      };
+      auto dq_mma = [&]() {   // dQ_i = dS K into the dP^T columns (issued after dK_i read them)
+        if (ptx::elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < BN / 16; ++kk)
             ptx::mma_ss(tbase + kDP, dSm + (uint64_t)(kk * 2048 >> 4), dKm + (uint64_t)(kk * 2048 >> 4),
                         id_mnmn, kk > 0);
           ptx::mma_commit(dq_full);
           ptx::mma_commit(ds_empty);
-          if (kPair)
-            ptx::mma_commit_mc(qdo_empty + (i & 1), kMask);   // this CTA released the stage, in all
-          else
-            ptx::mma_commit(qdo_empty + (i & 1));
         }
         __syncwarp();
       };
@@ -427,19 +434,24 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
             ptx::mma_commit(do_empty);
         }
         __syncwarp();
-        bool st_done = !more, dkq_done = false;
-        while (!st_done || !dkq_done) {
+        bool st_done = !more, dk_done = false, dq_done = false;
+        while (!st_done || !dq_done) {
           if (!st_done && ptx::mbar_try_wait(qdo_full + (s ^ 1), ((i + 1) >> 1) & 1)) {
             BTRACE4(11, i);
             ptx::tc_fence_after();
             st_mma(s ^ 1);
             st_done = true;
           }
-          if (!dkq_done && ptx::mbar_try_wait(ds_full, i & 1)) {
+          if (!dk_done && ptx::mbar_try_wait(dst_full, i & 1)) {
+            ptx::tc_fence_after();
+            dk_mma(i);
+            dk_done = true;
+          }
+          if (dk_done && !dq_done && ptx::mbar_try_wait(ds_full, i & 1)) {
             BTRACE4(1, i);
             ptx::tc_fence_after();
-            dkq_mma(i);
-            dkq_done = true;
+            dq_mma();
+            dq_done = true;
           }
         }
         if (more) {
@@ -534,10 +546,11 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
       ptx::tmem_wait_ld();
       ptx::reg_fence(rr);
       if (hq == 0) BTRACE4(20, i);
+      uint32_t pks[32];   // dS of both 32-query halves, packed bf16
 #pragma unroll
       for (int qc = 0; qc < 2; ++qc) {
         const uint32_t* r = rr + 32 * qc;
-        uint32_t pk[16];
+        uint32_t* pk = pks + 16 * qc;
 #pragma unroll
         for (int j4 = 0; j4 < 8; ++j4) {
           const float4 Dv = dst4[qc * 8 + j4];
@@ -552,21 +565,25 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
           pk[2 * j4] = ptx::pack_bf16(da.x, da.y);
           pk[2 * j4 + 1] = ptx::pack_bf16(db.x, db.y);
         }
-#ifdef BURST_EXP_NO_DS_STS   // experiment: dS never reaches SMEM (wrong results)
-        if (pk[0] == 0x7f7f7f7fu)
-#endif
+        // dS^T (bf16) over the dP^T columns this warpgroup has read, in the P^T layout:
+        // the A operand of dK from TMEM (32 KB less SMEM read per step)
+        ptx::tmem_st16(tbase + lane_off + kDP + 64 * hq + 16 * qc,
+                       *reinterpret_cast<const uint32_t(*)[16]>(pk));
+      }
+      ptx::tmem_wait_st();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(dst_full);   // dK_i may start while dS goes to SMEM for dQ_i
+#pragma unroll
+      for (int qc = 0; qc < 2; ++qc) {
+        const uint32_t* pk = pks + 16 * qc;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int ch = qc * 4 + u;   // 16-byte chunk (8 queries) of the 128 B swizzle row
           *reinterpret_cast<uint4*>(rowp + ((ch ^ (t & 7)) << 4)) =
               make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
         }
-        // dS^T (bf16) also over the dP^T columns this warpgroup has read, in the P^T
-        // layout: the A operand of dK from TMEM (32 KB less SMEM read per step)
-        ptx::tmem_st16(tbase + lane_off + kDP + 64 * hq + 16 * qc, pk);
       }
       if (hq == 0) BTRACE4(21, i);
-      ptx::tmem_wait_st();
       ptx::fence_proxy_async_smem();
       ptx::tc_fence_before();
       ptx::mbar_arrive(ds_full); if (hq == 0) BTRACE4(6, i); else BTRACE4(23, i);
