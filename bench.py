@@ -519,10 +519,10 @@ def run_ours(args, cfg, rank, world, local_rank):
                                "flops_per_launch": fwd_fl, "traffic": traffic_fwd}
     cpu = None
     if world == 1 and not args.skip_cpu:
-        dt, factor, kind = cpu_reference_sample(cfg, 1, args.ref_rows)
+        dt, factor, kind = cpu_reference_sample(cfg, 1, args.cpu_rows)
         ct = dt * factor
         cpu = {"value": B * N / ct, "unit": "tokens/s", "cores": cpu_threads(), "kind": kind,
-               "sample": f"{args.ref_rows} query rows x {N} keys x 1 head fwd+bwd ("
+               "sample": f"{args.cpu_rows} query rows x {N} keys x 1 head fwd+bwd ("
                          + ("stock burstsim.local_attn" if kind == "reference" else
                             "oracle port of the reference tiled algorithm")
                          + f", numpy fp32) in {dt:.2f}s, extrapolated x{factor:.0f}",
@@ -563,7 +563,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-rows", type=int, default=256)
+    ap.add_argument("--ref-rows", type=int, default=1024,
+                    help="query rows of the reference arm's per-step CPU sample (~3 s each)")
+    ap.add_argument("--cpu-rows", type=int, default=3072,
+                    help="query rows of the cpu_baseline sample in our line (~10 s of CPU work)")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--comm", default="nccl", choices=["nccl", "ce"],
                     help="ring transport at N>1: NCCL send/recv, or copy engines over CUDA IPC")
