@@ -1,4 +1,4 @@
-"""Seeded random pass configurations for the randomized parity sweep
+"""Seeded random pass configurations (128) for the randomized parity sweep
 (test_random_sweep.py): every option of run_ring_pass drawn together -- world size,
 causal / zigzag, batch and heads, head dim and dtype, padding, a block-sparse grid,
 backward payload, start offset, deterministic dQ -- so that combinations no
@@ -86,4 +86,5 @@ def pass_kwargs(case):
                 deterministic=case["deterministic"])
 
 
-CASES = [draw_case(s) for s in range(32)]
+CASES = [draw_case(s) for s in range(128)]   # the GPU sweep runs all
+CPU_CASES = CASES[:32]                          # the host-logic sweep the first 32

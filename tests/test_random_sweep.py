@@ -1,9 +1,9 @@
-"""Randomized parity sweep: 32 seeded run_ring_pass configurations (random_cases.py)
+"""Randomized parity sweep: 128 seeded run_ring_pass configurations (random_cases.py)
 that draw every pass option together, checked against the dense fp64 oracle.
 
 CPU (`-m "not gpu"`): the host side -- schedule, zigzag / padding, grid binding,
 start offset, both backward payloads, the folds -- driven by the oracle kernels
-(tests/oracle_kernels.py) in fp64, to 1e-9.
+(tests/oracle_kernels.py) in fp64, to 1e-9, on the first 32 cases.
 GPU (`-m gpu`): the same cases through the CUDA kernels: bf16 within 2e-2 max-abs of
 the oracle on the same rounded inputs (lse 1e-2), the f32 path within 1e-5 relative
 (BASELINE.json north star); deterministic cases also run twice and must agree bit
@@ -14,7 +14,7 @@ import numpy as np
 import pytest
 import torch
 
-from random_cases import CASES, dense_reference, pass_kwargs
+from random_cases import CASES, CPU_CASES, dense_reference, pass_kwargs
 
 IDS = [f"s{c['seed']}-{c['dtype']}-d{c['D']}-g{c['world']}"
        f"{'-causal' if c['causal'] else ''}{'-zz' if c['zigzag'] else ''}"
@@ -34,17 +34,17 @@ def _np(t):
 
 
 def test_cases_cover_every_option():
-    """The draw exercises each option at least a few times."""
+    """The draw exercises each option at least a few times, already in the CPU subset."""
     for key, want in (("causal", True), ("zigzag", True), ("pad", True),
                       ("deterministic", True), ("payload", "q")):
-        assert sum(c[key] == want for c in CASES) >= 3, key
-    assert sum(c["mask"] is not None for c in CASES) >= 5
-    assert sum(c["offset"] > 0 for c in CASES) >= 3
-    assert sum(c["dtype"] == "f32" for c in CASES) >= 4
-    assert {c["world"] for c in CASES} >= {1, 2, 3, 4, 5, 8}
+        assert sum(c[key] == want for c in CPU_CASES) >= 3, key
+    assert sum(c["mask"] is not None for c in CPU_CASES) >= 5
+    assert sum(c["offset"] > 0 for c in CPU_CASES) >= 3
+    assert sum(c["dtype"] == "f32" for c in CPU_CASES) >= 4
+    assert {c["world"] for c in CPU_CASES} >= {1, 2, 3, 4, 5, 8}
 
 
-@pytest.mark.parametrize("case", CASES, ids=IDS)
+@pytest.mark.parametrize("case", CPU_CASES, ids=IDS[:len(CPU_CASES)])
 def test_host_logic_random_case(case):
     from oracle_kernels import OracleKernels
 
