@@ -16,7 +16,7 @@ def _divisors(n, lo=1, hi=16):
     return [d for d in range(lo, hi + 1) if n % d == 0]
 
 
-def draw_case(seed: int) -> dict:
+def draw_case(seed: int, large: bool = False) -> dict:
     r = np.random.default_rng(1000 + seed)
     f32 = r.random() < 0.25
     D = int(r.choice([16, 32, 64])) if f32 else int(r.choice([64, 128]))
@@ -25,7 +25,8 @@ def draw_case(seed: int) -> dict:
     zigzag = bool(causal and world > 1 and r.random() < 0.7)
     pad = bool(r.random() < 0.3)
     unit = 2 * world * (1 if f32 else 8) if zigzag else world
-    n_total = unit * int(r.integers(max(1, 96 // unit), max(2, 1200 // unit)))
+    lo, hi = (2048, 6144) if large else (96, 1200)
+    n_total = unit * int(r.integers(max(1, lo // unit), max(2, hi // unit)))
     N = n_total
     if pad and unit > 1:
         # a length that is not a multiple of the unit; the pass zero-pads it to n_total,
@@ -51,7 +52,7 @@ def draw_case(seed: int) -> dict:
     return {
         "seed": seed, "dtype": "f32" if f32 else "bf16", "D": D, "world": world,
         "causal": causal, "zigzag": zigzag, "pad": pad, "N": N, "n_total": n_total,
-        "B": int(r.choice([1, 2])), "H": int(r.choice([1, 2, 3])),
+        "B": 1 if large else int(r.choice([1, 2])), "H": 1 if large else int(r.choice([1, 2, 3])),
         "payload": str(r.choice(["kv", "q"])),
         "offset": int(r.integers(0, world)) if world > 1 and r.random() < 0.4 else 0,
         "mask": mask,
@@ -88,3 +89,6 @@ def pass_kwargs(case):
 
 CASES = [draw_case(s) for s in range(128)]   # the GPU sweep runs all
 CPU_CASES = CASES[:32]                          # the host-logic sweep the first 32
+# multi-tile lengths (2K-6K tokens, one head): long key-tile walks, odd tile counts per
+# cluster pair, several query tiles per rank
+LARGE_CASES = [draw_case(s, large=True) for s in range(500, 524)]

@@ -4,6 +4,7 @@ that draw every pass option together, checked against the dense fp64 oracle.
 CPU (`-m "not gpu"`): the host side -- schedule, zigzag / padding, grid binding,
 start offset, both backward payloads, the folds -- driven by the oracle kernels
 (tests/oracle_kernels.py) in fp64, to 1e-9, on the first 32 cases.
+GPU also runs 24 multi-tile cases (2K-6K tokens, one head).
 GPU (`-m gpu`): the same cases through the CUDA kernels: bf16 within 2e-2 max-abs of
 the oracle on the same rounded inputs (lse 1e-2), the f32 path within 1e-5 relative
 (BASELINE.json north star); deterministic cases also run twice and must agree bit
@@ -14,13 +15,18 @@ import numpy as np
 import pytest
 import torch
 
-from random_cases import CASES, CPU_CASES, dense_reference, pass_kwargs
+from random_cases import CASES, CPU_CASES, LARGE_CASES, dense_reference, pass_kwargs
 
-IDS = [f"s{c['seed']}-{c['dtype']}-d{c['D']}-g{c['world']}"
-       f"{'-causal' if c['causal'] else ''}{'-zz' if c['zigzag'] else ''}"
-       f"{'-pad' if c['pad'] else ''}{'-grid' if c['mask'] else ''}-{c['payload']}"
-       f"{'-off%d' % c['offset'] if c['offset'] else ''}{'-det' if c['deterministic'] else ''}"
-       for c in CASES]
+
+def _id(c):
+    return (f"s{c['seed']}-{c['dtype']}-d{c['D']}-g{c['world']}"
+            f"{'-causal' if c['causal'] else ''}{'-zz' if c['zigzag'] else ''}"
+            f"{'-pad' if c['pad'] else ''}{'-grid' if c['mask'] else ''}-{c['payload']}"
+            f"{'-off%d' % c['offset'] if c['offset'] else ''}"
+            f"{'-det' if c['deterministic'] else ''}-n{c['N']}")
+
+
+IDS = [_id(c) for c in CASES]
 
 
 def _inputs(case, dtype, device):
@@ -62,7 +68,7 @@ def test_host_logic_random_case(case):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", CASES, ids=IDS)
+@pytest.mark.parametrize("case", CASES + LARGE_CASES, ids=IDS + [_id(c) for c in LARGE_CASES])
 def test_gpu_random_case(case):
     from gpu_utils import poison_allocator
 
