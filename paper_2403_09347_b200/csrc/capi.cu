@@ -290,13 +290,18 @@ int launch_bwd4_bf16(const burst_hop* h, const void* q, const void* k, const voi
     if ((rc = make_tmap(&p.tm_q64, q, h->n_q, h->heads, D, h->batch, 64))) return rc;
     if ((rc = make_tmap(&p.tm_do64, dout, h->n_q, h->heads, D, h->batch, 64))) return rc;
   }
-  if (h->dq_order)
+  if constexpr (kCl > 1) {
+    if (h->dq_order)   // deterministic: the pairs walk in key-tile order like single CTAs
+      rc = h->grid_skip ? go_pair(bwd4::lao_bwd4_kernel<D, true, true, kCl>)
+                        : go_pair(bwd4::lao_bwd4_kernel<D, false, true, kCl>);
+    else
+      rc = h->grid_skip ? go_pair(bwd4::lao_bwd4_kernel<D, true, false, kCl>)
+                        : go_pair(bwd4::lao_bwd4_kernel<D, false, false, kCl>);
+  } else if (h->dq_order) {
     rc = h->grid_skip ? go(bwd4::lao_bwd4_kernel<D, true, true>) : go(bwd4::lao_bwd4_kernel<D, false, true>);
-  else if constexpr (kCl > 1)
-    rc = h->grid_skip ? go_pair(bwd4::lao_bwd4_kernel<D, true, false, kCl>)
-                      : go_pair(bwd4::lao_bwd4_kernel<D, false, false, kCl>);
-  else
+  } else {
     rc = h->grid_skip ? go(bwd4::lao_bwd4_kernel<D, true, false>) : go(bwd4::lao_bwd4_kernel<D, false, false>);
+  }
   if (rc) return rc;
   CHECK_LAUNCH();
   return BURST_OK;
