@@ -104,6 +104,13 @@ int* device_flags() {
   return flags[dev];
 }
 
+#ifdef BURST_LIFE
+unsigned long long* life_buffer() {
+  static unsigned long long* buf = nullptr;
+  if (!buf) cudaMalloc(&buf, 65536 * 8 * sizeof(unsigned long long));
+  return buf;
+}
+#endif
 #ifdef BURST_TRACE
 long long* trace_buffer() {
   static long long* buf = nullptr;
@@ -272,6 +279,9 @@ int launch_bwd4_bf16(const burst_hop* h, const void* q, const void* k, const voi
 #ifdef BURST_TRACE
   p.trace = trace_buffer();
 #endif
+#ifdef BURST_LIFE
+  p.life = life_buffer();
+#endif
   dim3 grid((unsigned)ceil_div(h->k_len, bwd4::BN), h->heads, h->batch);
   auto go = [&](auto kernel) -> int {
     if (int e = set_smem(kernel, bwd4::Cfg<D>::kSmemBytes)) return e;
@@ -343,6 +353,13 @@ int check_dims(int dtype, int B, int H, int D, int64_t n) {
 
 }  // namespace
 
+#ifdef BURST_LIFE
+extern "C" __attribute__((visibility("default"))) int burst_exp_life_read(unsigned long long* host) {
+  cudaDeviceSynchronize();
+  return (int)cudaMemcpy(host, life_buffer(), 65536 * 8 * sizeof(unsigned long long),
+                         cudaMemcpyDeviceToHost);
+}
+#endif
 #ifdef BURST_TRACE
 extern "C" __attribute__((visibility("default"))) int burst_exp_trace_read(long long* host) {
   cudaDeviceSynchronize();

@@ -74,6 +74,7 @@ struct Params {
   int accumulate;
   int* dq_order;      // deterministic mode: per-(b*h, query tile) count of finished key tiles
   long long* trace;   // BURST_TRACE builds only: per-iteration clock64 timeline
+  unsigned long long* life;   // BURST_LIFE builds only: per-CTA globaltimer events
 };
 
 // Deterministic dQ: the reductions into one query tile happen in ascending key-tile
@@ -108,6 +109,20 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 #else
 #define BTRACE4(ev, i)
 #endif
+#ifdef BURST_LIFE   // experiment: CTA lifetime events (globaltimer ns; slot 7 = SM id)
+#define BLIFE(ev)                                                                            \
+  do {                                                                                       \
+    unsigned long long t_;                                                                   \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                   \
+    const size_t c_ = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x; \
+    if (p.life && c_ < 65536) p.life[c_ * 8 + (ev)] = t_;                                    \
+    if ((ev) == 0 && p.life && c_ < 65536) {                                                 \
+      unsigned s_; asm volatile("mov.u32 %0, %%smid;" : "=r"(s_)); p.life[c_ * 8 + 7] = s_;  \
+    }                                                                                        \
+  } while (0)
+#else
+#define BLIFE(ev)
+#endif
 
 // kGrid: the hop carries a block-sparse grid mask (tile skipping + element masks);
 // the instantiation without it keeps the dense loops free of the skip bookkeeping.
@@ -130,6 +145,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
   // the runtime check below can then only fail on a toolchain that ignores it, in
   // which case the launch reports a CudaError (flag bit 2) instead of trapping.
   extern __shared__ __align__(1024) uint8_t smem_raw[];
+  if (threadIdx.x == 0) BLIFE(0);
   uint8_t* smem;
   {
     const uint32_t s = ptx::smem_u32(smem_raw);
@@ -276,6 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
   else
     __syncthreads();
   ptx::tc_fence_after();
+  if (threadIdx.x == 0) BLIFE(1);
   const uint32_t tbase = *tmem_holder;
   if (kGrid) nlive = (int)tmem_holder[1];
   constexpr uint32_t kS = 0, kDP = 128, kDV = 256, kDK = 256 + D;
@@ -492,6 +509,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
       const bool warp_full = __all_sync(0xffffffffu, lo == 0 && hi == 64 && gq == 0);
       ptx::mbar_wait(qdo_full + s, (i >> 1) & 1);
       ptx::mbar_wait(s_full, i & 1); if (hq == 0) BTRACE4(3, i);
+      if (i == 0 && threadIdx.x == 0) BLIFE(2);
       ptx::tc_fence_after();
       const float4* lse4 = reinterpret_cast<const float4*>(sStat + s * 2 * BM) + 16 * hq;
       const float4* dst4 = lse4 + BM / 4;
@@ -703,15 +721,18 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
         order_wait(turn(walked), me);
         order_publish(turn(walked), me + 1);
       }
+    if (t == 0) BLIFE(3);
     if (t == 0) ptx::bulk_wait_all();
   }
 
   __syncwarp();
+  if (threadIdx.x == 0) BLIFE(4);
   ptx::tc_fence_before();
   if (kPair)
     ptx::cluster_sync();   // no multicast load or remote arrive may target an exited CTA
   else
     __syncthreads();
+  if (threadIdx.x == 0) BLIFE(5);
   if (warp == 12) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tbase, 512);
