@@ -1,0 +1,10 @@
+# deterministic dQ, publish deferred by one tile: parity + A/B vs the previous ordered drain
+timeout 600 python -m pytest tests/test_gpu_deterministic.py tests/test_random_sweep.py -m gpu -q -x > gpurun_out/detdefer_tests.log 2>&1; echo rc=$? >> gpurun_out/detdefer_tests.log
+tail -3 gpurun_out/detdefer_tests.log
+for i in 1 2; do
+  timeout 300 python exp/time_kernels.py c3 det
+  BURST_LIB=exp/lib_det_prev.so timeout 300 python exp/time_kernels.py c3 det
+done 2>&1 | grep -v Warn | tee gpurun_out/detdefer_ab.txt
+timeout 300 python exp/time_kernels.py c3 causal det 2>&1 | tee -a gpurun_out/detdefer_ab.txt
+timeout 300 python exp/time_kernels.py c2 det 2>&1 | tee -a gpurun_out/detdefer_ab.txt
+timeout 300 python exp/time_kernels.py c3 2>&1 | tee -a gpurun_out/detdefer_ab.txt
