@@ -3,7 +3,7 @@ timeout 600 python -m pytest tests/test_gpu_deterministic.py tests/test_random_s
 tail -3 gpurun_out/detdefer_tests.log
 for i in 1 2; do
   timeout 300 python exp/time_kernels.py c3 det
-  BURST_LIB=exp/lib_det_prev.so timeout 300 python exp/time_kernels.py c3 det
+  BURST_LIB=exp/lib_prev.so timeout 300 python exp/time_kernels.py c3 det
 done 2>&1 | grep -v Warn | tee gpurun_out/detdefer_ab.txt
 timeout 300 python exp/time_kernels.py c3 causal det 2>&1 | tee -a gpurun_out/detdefer_ab.txt
 timeout 300 python exp/time_kernels.py c2 det 2>&1 | tee -a gpurun_out/detdefer_ab.txt
