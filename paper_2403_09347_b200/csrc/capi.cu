@@ -107,7 +107,7 @@ int* device_flags() {
 #ifdef BURST_LIFE
 unsigned long long* life_buffer() {
   static unsigned long long* buf = nullptr;
-  if (!buf) cudaMalloc(&buf, 65536 * 8 * sizeof(unsigned long long));
+  if (!buf) { cudaMalloc(&buf, 65536 * 16 * sizeof(unsigned long long)); cudaMemset(buf, 0, 65536 * 16 * sizeof(unsigned long long)); }
   return buf;
 }
 #endif
@@ -356,7 +356,7 @@ int check_dims(int dtype, int B, int H, int D, int64_t n) {
 #ifdef BURST_LIFE
 extern "C" __attribute__((visibility("default"))) int burst_exp_life_read(unsigned long long* host) {
   cudaDeviceSynchronize();
-  return (int)cudaMemcpy(host, life_buffer(), 65536 * 8 * sizeof(unsigned long long),
+  return (int)cudaMemcpy(host, life_buffer(), 65536 * 16 * sizeof(unsigned long long),
                          cudaMemcpyDeviceToHost);
 }
 #endif

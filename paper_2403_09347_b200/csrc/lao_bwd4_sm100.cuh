@@ -109,15 +109,16 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 #else
 #define BTRACE4(ev, i)
 #endif
-#ifdef BURST_LIFE   // experiment: CTA lifetime events (globaltimer ns; slot 7 = SM id)
+#ifdef BURST_LIFE   // experiment: CTA lifetime events (globaltimer ns; slot 7 = SM id, 8/9 = ordered-mode
+                    // turn waits in the first 32 live tiles / after them)
 #define BLIFE(ev)                                                                            \
   do {                                                                                       \
     unsigned long long t_;                                                                   \
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                   \
     const size_t c_ = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x; \
-    if (p.life && c_ < 65536) p.life[c_ * 8 + (ev)] = t_;                                    \
+    if (p.life && c_ < 65536) p.life[c_ * 16 + (ev)] = t_;                                    \
     if ((ev) == 0 && p.life && c_ < 65536) {                                                 \
-      unsigned s_; asm volatile("mov.u32 %0, %%smid;" : "=r"(s_)); p.life[c_ * 8 + 7] = s_;  \
+      unsigned s_; asm volatile("mov.u32 %0, %%smid;" : "=r"(s_)); p.life[c_ * 16 + 7] = s_;  \
     }                                                                                        \
   } while (0)
 #else
@@ -653,6 +654,9 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
     auto turn = [&](int u) -> int* { return p.dq_order + bh * NTq + qtile(u) / BM; };
     const int me = (int)blockIdx.x;
     int walked = 0;   // walk indices below this have been published (ordered mode)
+#ifdef BURST_LIFE
+    unsigned long long wait_a = 0, wait_b = 0;
+#endif
     for (int i = 0, ti = next_live(0); i < nlive; ++i, ti = next_live(ti + 1)) {
       const int64_t q0 = qtile(ti);
       const bool qvalid = q0 + t >= hp.q_begin && q0 + t < q_end && q0 + t < hp.n_q;
@@ -661,7 +665,16 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
           order_wait(turn(walked), me);
           order_publish(turn(walked), me + 1);
         }
+#ifdef BURST_LIFE
+        unsigned long long w0_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w0_));
+#endif
         order_wait(turn(ti), me);
+#ifdef BURST_LIFE
+        unsigned long long w1_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w1_));
+        (i < 32 ? wait_a : wait_b) += w1_ - w0_;
+#endif
       }
       ptx::mbar_wait(dq_full, i & 1); BTRACE4(7, i);
       ptx::tc_fence_after();
@@ -722,6 +735,12 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
         order_publish(turn(walked), me + 1);
       }
     if (t == 0) BLIFE(3);
+#ifdef BURST_LIFE
+    if (t == 0 && p.life) {
+      const size_t c_ = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+      if (c_ < 65536) { p.life[c_ * 16 + 8] = wait_a; p.life[c_ * 16 + 9] = wait_b; }
+    }
+#endif
     if (t == 0) ptx::bulk_wait_all();
   }
 
