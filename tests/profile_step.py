@@ -25,7 +25,7 @@ q, k, v, do = (torch.randn(B, N, H, D, device="cuda", dtype=torch.bfloat16) for 
 for t in (q, k, v):
     t.requires_grad_(True)
 for _ in range(a.steps):
-    o, lse = burst_attn_func(q, k, v, causal=cfg["causal"])
+    o, lse = burst_attn_func(q, k, v, causal=cfg["causal"], mask=cfg.get("mask"))
     torch.autograd.grad(o, (q, k, v), do)
 torch.cuda.synchronize()
 print("done")
