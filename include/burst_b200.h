@@ -88,11 +88,13 @@ typedef struct {
    * key -> MaskError), bit 1 (non-finite output -> NonFiniteError), bit 2 (launch
    * could not run -> CudaError). */
   int32_t* flags;
-  /* Deterministic dQ (optional): device int32 array of batch * heads * ceil(n_q/128)
-   * words.  burst_lao_bwd zeroes it on the stream and then reduces every 128-row dQ
-   * tile in ascending key-tile order, so gradients are bit-reproducible run to run
-   * (the reference's bitwise executor equivalence, pkg/tests/test_sim.py:280-295).
-   * NULL = fastest (unordered fp32 reductions).  The f32 path is always ordered. */
+  /* Deterministic gradients (optional): non-NULL selects the bit-reproducible bf16
+   * backward (the reference's bitwise executor equivalence, pkg/tests/test_sim.py:
+   * 280-295): burst_lao_bwd then computes dK/dV in the key-stationary kernel and dQ in
+   * a query-stationary kernel that accumulates each dQ row over the key tiles in order
+   * and adds it to dq_acc once -- no order-dependent fp32 reduction is left.  The
+   * device int32 array (batch * heads * ceil(n_q/128) words) is reserved scratch.
+   * NULL = fastest (unordered fp32 dQ reductions).  The f32 path is always ordered. */
   int32_t* dq_order;
   /* Key-tile visiting order of the bf16 forward (optional; local_forward_tiled's
    * key_tile_order, local_attn.py:212-225): device int32 permutation of the hop's

@@ -20,7 +20,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libburst_b200.so")
 SOURCES = ["capi.cu", "ring_nccl.cu", "ring_ipc.cu"]
-HEADERS = ["ptx.cuh", "common.cuh", "lao_fwd_sm100.cuh", "lao_bwd4_sm100.cuh",
+HEADERS = ["ptx.cuh", "common.cuh", "lao_fwd_sm100.cuh", "lao_bwd4_sm100.cuh", "lao_dq_sm100.cuh",
            "simt_f32.cuh", "aux_kernels.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

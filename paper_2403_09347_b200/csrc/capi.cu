@@ -16,6 +16,7 @@
 #include "../../include/burst_b200.h"
 #include "aux_kernels.cuh"
 #include "lao_bwd4_sm100.cuh"
+#include "lao_dq_sm100.cuh"
 #include "lao_fwd_sm100.cuh"
 #include "simt_f32.cuh"
 
@@ -256,6 +257,35 @@ int launch_fwd_f32(const burst_hop* h, const void* q, const void* k, const void*
   return BURST_OK;
 }
 
+// Deterministic dQ (query-stationary, one writer per dQ row; lao_dq_sm100.cuh).
+template <int D>
+int launch_dq_bf16(const burst_hop* h, const void* q, const void* k, const void* v, const void* dout,
+                   const float* stats, float* dq_acc, cudaStream_t st) {
+  bdq::Params p;
+  memset(&p, 0, sizeof(p));
+  int rc;
+  if ((rc = make_tmap(&p.tm_q, q, h->n_q, h->heads, D, h->batch))) return rc;
+  if ((rc = make_tmap(&p.tm_do, dout, h->n_q, h->heads, D, h->batch))) return rc;
+  if ((rc = make_tmap(&p.tm_k, k, h->n_k, h->heads, D, h->batch))) return rc;
+  if ((rc = make_tmap(&p.tm_v, v, h->n_k, h->heads, D, h->batch))) return rc;
+  p.stats = stats;
+  p.dq_acc = dq_acc;
+  p.hop = *h;
+  p.hop.flags = flags_of(h);
+  p.scale_log2 = h->softmax_scale * kLog2e;
+  p.scale = h->softmax_scale;
+  dim3 grid((unsigned)ceil_div(h->q_len, bdq::BM), h->heads, h->batch);
+  auto go = [&](auto kernel) -> int {
+    if (int e = set_smem(kernel, bdq::Cfg<D>::kSmemBytes)) return e;
+    kernel<<<grid, bdq::kThreads, bdq::Cfg<D>::kSmemBytes, st>>>(p);
+    return BURST_OK;
+  };
+  rc = h->grid_skip ? go(bdq::lao_dq_kernel<D, true>) : go(bdq::lao_dq_kernel<D, false>);
+  if (rc) return rc;
+  CHECK_LAUNCH();
+  return BURST_OK;
+}
+
 template <int D>
 int launch_bwd4_bf16(const burst_hop* h, const void* q, const void* k, const void* v, const void* dout,
                      const float* stats, float* dq_acc, float* dk, float* dv, int acc, cudaStream_t st) {
@@ -272,10 +302,6 @@ int launch_bwd4_bf16(const burst_hop* h, const void* q, const void* k, const voi
   p.scale_log2 = h->softmax_scale * kLog2e;
   p.scale = h->softmax_scale;
   p.accumulate = acc;
-  p.dq_order = h->dq_order;
-  if (h->dq_order)
-    CUDA_TRY(cudaMemsetAsync(h->dq_order, 0, sizeof(int32_t) * (size_t)h->batch * h->heads *
-                                                 (size_t)ceil_div(h->n_q, bwd4::BM), st));
 #ifdef BURST_TRACE
   p.trace = trace_buffer();
 #endif
@@ -301,7 +327,7 @@ int launch_bwd4_bf16(const burst_hop* h, const void* q, const void* k, const voi
     if ((rc = make_tmap(&p.tm_do64, dout, h->n_q, h->heads, D, h->batch, 64))) return rc;
   }
   if constexpr (kCl > 1) {
-    if (h->dq_order)   // deterministic: the pairs walk in key-tile order like single CTAs
+    if (h->dq_order)   // deterministic: dK/dV only (dQ from lao_dq below)
       rc = h->grid_skip ? go_pair(bwd4::lao_bwd4_kernel<D, true, true, kCl>)
                         : go_pair(bwd4::lao_bwd4_kernel<D, false, true, kCl>);
     else
@@ -314,6 +340,7 @@ int launch_bwd4_bf16(const burst_hop* h, const void* q, const void* k, const voi
   }
   if (rc) return rc;
   CHECK_LAUNCH();
+  if (h->dq_order) return launch_dq_bf16<D>(h, q, k, v, dout, stats, dq_acc, st);
   return BURST_OK;
 }
 

@@ -72,25 +72,9 @@ struct Params {
   burst_hop hop;
   float scale_log2, scale;
   int accumulate;
-  int* dq_order;      // deterministic mode: per-(b*h, query tile) count of finished key tiles
   long long* trace;   // BURST_TRACE builds only: per-iteration clock64 timeline
   unsigned long long* life;   // BURST_LIFE builds only: per-CTA globaltimer events
 };
-
-// Deterministic dQ: the reductions into one query tile happen in ascending key-tile
-// order.  Key tile j waits until dq_order[tile] == j, reduces, and publishes j + 1 once
-// its bulk reductions have completed (async-proxy writes ordered before the release).
-__device__ __forceinline__ void order_wait(const int* w, int want) {
-  int v;
-  do {
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(w) : "memory");
-  } while (v != want);
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-__device__ __forceinline__ void order_publish(int* w, int val) {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(w), "r"(val) : "memory");
-}
 
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -109,8 +93,7 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 #else
 #define BTRACE4(ev, i)
 #endif
-#ifdef BURST_LIFE   // experiment: CTA lifetime events (globaltimer ns; slot 7 = SM id, 8/9 = ordered-mode
-                    // turn waits in the first 32 live tiles / after them)
+#ifdef BURST_LIFE   // experiment: CTA lifetime events (globaltimer ns; slot 7 = SM id)
 #define BLIFE(ev)                                                                            \
   do {                                                                                       \
     unsigned long long t_;                                                                   \
@@ -127,8 +110,10 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 
 // kGrid: the hop carries a block-sparse grid mask (tile skipping + element masks);
 // the instantiation without it keeps the dense loops free of the skip bookkeeping.
-// kOrdered: deterministic dQ (p.dq_order set); its own instantiation keeps the turn
-// bookkeeping out of the drain's register budget in the default kernel.
+// kOrdered: deterministic mode (p.dq_order set) -- dK/dV only; dQ is computed by the
+// query-stationary lao_dq kernel (lao_dq_sm100.cuh), one writer per dQ row, so no
+// order-dependent fp32 reduction remains.  The dS SMEM stores, the dQ MMA and the
+// drain are compiled out; dP^T_{i+1} waits for dK_i (the last reader of dS^T).
 // kCl (cluster size 1, 2 or 4): launched as kCl-CTA clusters over consecutive key tiles
 // that walk the SAME query tiles; each CTA TMA-loads 1/kCl of every Q and dO tile (a
 // 64-column box, or a 64-row half of one for kCl = 4) and multicasts it to all (1/kCl
@@ -209,11 +194,9 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
   const int nq = qs < q_end ? (int)ceil_div(q_end - qs, BM) : 0;
   // Query-tile order rotated per CTA: concurrently resident CTAs (consecutive key
   // tiles of one head) reduce into different dQ tiles (measured best at 128K,
-  // profiles/r01_rotation_exp.txt).  Deterministic mode walks the tiles in order
-  // (key tile j follows j - 1 through every tile).
-  constexpr bool ordered = kOrdered;
+  // profiles/r01_rotation_exp.txt).
   const unsigned walker = blockIdx.x / kCl;
-  const int rot = (nq > 0 && !ordered) ? (int)((walker * (unsigned)BURST_BWD_ROT) % (unsigned)nq) : 0;
+  const int rot = nq > 0 ? (int)((walker * (unsigned)BURST_BWD_ROT) % (unsigned)nq) : 0;
   auto qtile = [&](int i) -> int64_t { int j = i + rot; if (j >= nq) j -= nq; return qs + (int64_t)j * BM; };
   // Block-sparse grid: query tiles whose every (query, key) pair with this CTA's keys
   // lies in skipped cells are skipped by every role.  Roles count LIVE tiles (stages,
@@ -414,6 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
             ptx::mma_commit_mc(qdo_empty + (i & 1), kMask);   // this CTA released the stage, in all
           else
             ptx::mma_commit(qdo_empty + (i & 1));
+          if (kOrdered) ptx::mma_commit(dq_full);   // dS^T read: the dP^T columns are free
         }
         __syncwarp();
       };
@@ -464,6 +448,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
             ptx::tc_fence_after();
             dk_mma(i);
             dk_done = true;
+            if (kOrdered) dq_done = true;
           }
           if (dk_done && !dq_done && ptx::mbar_try_wait(ds_full, i & 1)) {
             BTRACE4(1, i);
@@ -473,7 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
           }
         }
         if (more) {
-          ptx::mbar_wait(dq_empty, i & 1); BTRACE4(2, i);
+          ptx::mbar_wait(kOrdered ? dq_full : dq_empty, i & 1); BTRACE4(2, i);
           ptx::mbar_wait(do_full, (i + 1) & 1); BTRACE4(10, i);
           ptx::tc_fence_after();
           dpt_mma();
@@ -555,7 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
       ptx::mbar_arrive(p_full); if (hq == 0) BTRACE4(4, i); else BTRACE4(22, i);
 
       ptx::mbar_wait(dp_full, i & 1); if (hq == 0) BTRACE4(5, i);
-      ptx::mbar_wait(ds_empty, (i & 1) ^ 1);
+      if (!kOrdered) ptx::mbar_wait(ds_empty, (i & 1) ^ 1);
       ptx::tc_fence_after();
       uint8_t* rowp = sdS + hq * 16384 + t * 128;   // SW128 K-major box of this query half
       // both 32-column halves of this warpgroup's dP^T in one TMEM round trip
@@ -592,6 +577,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
       ptx::mbar_arrive(dst_full);   // dK_i may start while dS goes to SMEM for dQ_i
+      if (kOrdered) continue;       // deterministic mode: dQ comes from lao_dq
 #pragma unroll
       for (int qc = 0; qc < 2; ++qc) {
         const uint32_t* pk = pks + 16 * qc;
@@ -650,32 +636,9 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
     const int t = threadIdx.x & 127;           // query row within the tile
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     float4* stg = reinterpret_cast<float4*>(sStage);
-    // deterministic mode: this CTA's turn word of query tile u (walk index)
-    auto turn = [&](int u) -> int* { return p.dq_order + bh * NTq + qtile(u) / BM; };
-    const int me = (int)blockIdx.x;
-    int walked = 0;   // walk indices below this have been published (ordered mode)
-#ifdef BURST_LIFE
-    unsigned long long wait_a = 0, wait_b = 0;
-#endif
-    for (int i = 0, ti = next_live(0); i < nlive; ++i, ti = next_live(ti + 1)) {
+    for (int i = 0, ti = next_live(0); i < (kOrdered ? 0 : nlive); ++i, ti = next_live(ti + 1)) {
       const int64_t q0 = qtile(ti);
       const bool qvalid = q0 + t >= hp.q_begin && q0 + t < q_end && q0 + t < hp.n_q;
-      if (ordered && t == 0) {   // before the TMEM load: no tile registers live here
-        for (; walked < ti; ++walked) {   // grid-skipped tiles: pass the turn on
-          order_wait(turn(walked), me);
-          order_publish(turn(walked), me + 1);
-        }
-#ifdef BURST_LIFE
-        unsigned long long w0_;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w0_));
-#endif
-        order_wait(turn(ti), me);
-#ifdef BURST_LIFE
-        unsigned long long w1_;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(w1_));
-        (i < 32 ? wait_a : wait_b) += w1_ - w0_;
-#endif
-      }
       ptx::mbar_wait(dq_full, i & 1); BTRACE4(7, i);
       ptx::tc_fence_after();
       uint32_t r[D];
@@ -722,25 +685,9 @@ __global__ void __launch_bounds__(kThreads, 1) lao_bwd4_kernel(const __grid_cons
           ptx::bulk_commit();
         }
       }
-      if (ordered && t == 0) {
-        ptx::bulk_wait_all();
-        order_publish(turn(ti), me + 1);
-        walked = ti + 1;
-      }
       BTRACE4(9, i);
     }
-    if (ordered && t == 0)
-      for (; walked < nq; ++walked) {
-        order_wait(turn(walked), me);
-        order_publish(turn(walked), me + 1);
-      }
     if (t == 0) BLIFE(3);
-#ifdef BURST_LIFE
-    if (t == 0 && p.life) {
-      const size_t c_ = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-      if (c_ < 65536) { p.life[c_ * 16 + 8] = wait_a; p.life[c_ * 16 + 9] = wait_b; }
-    }
-#endif
     if (t == 0) ptx::bulk_wait_all();
   }
 

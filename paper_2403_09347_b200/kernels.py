@@ -88,7 +88,7 @@ class BwdState:
     stats: torch.Tensor   # flat [2][B*H][ceil(n/128)*128] (lse*log2e, D)
     dq_acc: torch.Tensor  # TL fp32
     flags: torch.Tensor   # [1] int32 error word of the pass
-    order: torch.Tensor | None = None   # deterministic mode: burst_hop.dq_order words
+    order: torch.Tensor | None = None   # deterministic mode: burst_hop.dq_order (selector)
 
 
 # bits of the device error word (include/burst_b200.h burst_hop.flags)
@@ -253,7 +253,7 @@ class CudaKernels:
     # ------------------------------------------------------------ backward
     def bwd_prepare(self, o, dout, lse, stream=None, deterministic: bool = False) -> BwdState:
         """Backward stats + zeroed dQ accumulator of the pinned block; `deterministic`
-        also allocates the dQ turn words (bit-reproducible dQ reductions)."""
+        also selects the bit-reproducible backward (dK/dV key-stationary, dQ query-stationary)."""
         B, n, H, D = o.shape
         nt = -(-n // 128) * 128
         with torch.cuda.stream(stream) if stream is not None else _nullctx():

@@ -3,9 +3,10 @@
 The reference's passes are bitwise equal across executors, overlap modes and injected
 delays (pkg/tests/test_sim.py:280-310).  Here the only order-dependent arithmetic is
 the fp32 dQ reduction of the bf16 backward (many key tiles add into one dQ tile); with
-`deterministic=True` every dQ tile is reduced in ascending key-tile order, so repeated
-passes -- and passes whose CTAs are scheduled differently because another kernel
-shares the GPU -- give identical bits, and still match the oracle.
+`deterministic=True` dQ comes from a query-stationary kernel that accumulates each row
+over the key tiles in order and writes it once, so repeated passes -- and passes whose
+CTAs are scheduled differently because another kernel shares the GPU -- give
+identical bits, and still match the oracle.
 """
 
 import pytest
@@ -65,8 +66,8 @@ def test_deterministic_backward_is_bitwise_reproducible(N, world, causal, zigzag
 
 
 def test_deterministic_grid_mask_passes_turns_over_skipped_tiles():
-    """Block-sparse grid: key tiles with no live query tile still hand every dQ
-    tile's turn on (a missed hand-off would hang the launch)."""
+    """Block-sparse grid: tiles dead for a query tile are skipped by the
+    query-stationary dQ kernel and by the dK/dV kernel alike, bit-reproducibly."""
     spec = {"n_query_blocks": 8, "n_key_blocks": 8,
             "skip": [[0, 1], [0, 2], [0, 3], [3, 0], [5, 5], [7, 2], [6, 0], [6, 1]]}
     from test_gpu_lao import _grid_oracle
