@@ -33,9 +33,11 @@ struct Cfg {
   static constexpr int kBoxBytes = 128 * 64 * 2;
   static constexpr int kBoxes = D / 64;
   static constexpr int kTileBytes = kBoxBytes * kBoxes;
-  static constexpr int kStages = 2;          // K_j + V_j per stage
+  // K_j and V_j occupy one slot each (items 2j, 2j+1 of the load stream): V_j is free
+  // after dP_j, K_j after dQ_j, so the loads run up to two tiles ahead of the MMAs
+  static constexpr int kSlots = (D == 128) ? 5 : 8;
   static constexpr int kLiveWords = 256;     // live-key-tile bitmap (grid masks): 8192 tiles
-  static constexpr int kSmemBytes = 1024 + 2 * kTileBytes + kStages * 2 * kTileBytes + 256 +
+  static constexpr int kSmemBytes = 1024 + 2 * kTileBytes + kSlots * kTileBytes + 256 +
                                     4 * kLiveWords;
 };
 
@@ -58,12 +60,12 @@ __global__ void __launch_bounds__(kThreads, 1) lao_dq_kernel(const __grid_consta
   }
   uint8_t* sQ = smem;
   uint8_t* sdO = sQ + C::kTileBytes;
-  uint8_t* sKV = sdO + C::kTileBytes;   // stage s: K at s*2*tile, V at s*2*tile + tile
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::kStages * 2 * C::kTileBytes);
+  uint8_t* sKV = sdO + C::kTileBytes;   // kSlots slots: K_j, V_j alternate
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::kSlots * C::kTileBytes);
   uint64_t* q_full = bars;                       // Q and dO landed
-  uint64_t* kv_full = bars + 1;                  // [kStages]
-  uint64_t* kv_empty = kv_full + C::kStages;     // [kStages]
-  uint64_t* s_full = kv_empty + C::kStages;      // [2] S_b computed
+  uint64_t* kv_full = bars + 1;                  // [kSlots]
+  uint64_t* kv_empty = kv_full + C::kSlots;      // [kSlots]
+  uint64_t* s_full = kv_empty + C::kSlots;       // [2] S_b computed
   uint64_t* s_free = s_full + 2;                 // [2] dQ MMA done reading dS in S_b
   uint64_t* ds_full = s_free + 2;                // [2] dS in S_b (256 arrivals)
   uint64_t* dp_full = ds_full + 2;
@@ -127,7 +129,7 @@ __global__ void __launch_bounds__(kThreads, 1) lao_dq_kernel(const __grid_consta
   if (warp == 8) {
     if (lane == 0) {
       ptx::mbar_init(q_full, 1);
-      for (int s = 0; s < C::kStages; ++s) {
+      for (int s = 0; s < C::kSlots; ++s) {
         ptx::mbar_init(kv_full + s, 1);
         ptx::mbar_init(kv_empty + s, 1);
       }
@@ -165,17 +167,16 @@ __global__ void __launch_bounds__(kThreads, 1) lao_dq_kernel(const __grid_consta
           ptx::tma_load_4d(sdO + x * C::kBoxBytes, &p.tm_do, q_full, x * 64, h, (int)row0, b);
         }
         int it = 0;
-        for (int u = first; u < nkv; u = next_live(u + 1), ++it) {
-          const int s = it % C::kStages;
-          const uint32_t use = it / C::kStages;
+        for (int u = first; u < nkv; u = next_live(u + 1)) {
           const int krow = (int)(hp.k_begin + (int64_t)u * BN);
-          ptx::mbar_wait(kv_empty + s, (use & 1) ^ 1);
-          ptx::mbar_expect_tx(kv_full + s, 2 * C::kTileBytes);
-          uint8_t* sk = sKV + s * 2 * C::kTileBytes;
-          for (int x = 0; x < C::kBoxes; ++x) {
-            ptx::tma_load_4d(sk + x * C::kBoxBytes, &p.tm_k, kv_full + s, x * 64, h, krow, b);
-            ptx::tma_load_4d(sk + C::kTileBytes + x * C::kBoxBytes, &p.tm_v, kv_full + s, x * 64, h,
-                             krow, b);
+          for (int kv = 0; kv < 2; ++kv, ++it) {
+            const int s = it % C::kSlots;
+            const uint32_t use = it / C::kSlots;
+            ptx::mbar_wait(kv_empty + s, (use & 1) ^ 1);
+            ptx::mbar_expect_tx(kv_full + s, C::kTileBytes);
+            for (int x = 0; x < C::kBoxes; ++x)
+              ptx::tma_load_4d(sKV + s * C::kTileBytes + x * C::kBoxBytes, kv == 0 ? &p.tm_k : &p.tm_v,
+                               kv_full + s, x * 64, h, krow, b);
           }
         }
       }
@@ -192,59 +193,65 @@ __global__ void __launch_bounds__(kThreads, 1) lao_dq_kernel(const __grid_consta
         const uint64_t dKVm = ptx::make_sdesc(ptx::smem_u32(sKV), C::kBoxBytes, 1024);
         constexpr uint64_t kTile = (uint64_t)(C::kTileBytes >> 4);
         auto kmaj = [](int kk) -> uint64_t { return (uint64_t)(((kk >> 2) * C::kBoxBytes + (kk & 3) * 32) >> 4); };
-        auto s_mma = [&](int buf, int stage) {   // S_buf = Q K^T
+        // item it of the load stream (K_j = 2j, V_j = 2j + 1): its slot and fill parity
+        auto slot = [](int it) -> int { return it % C::kSlots; };
+        auto wait_item = [&](int it) { ptx::mbar_wait(kv_full + slot(it), (it / C::kSlots) & 1); };
+        auto s_mma = [&](int buf, int jj) {   // S_buf = Q K_jj^T
           if (ptx::elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < D / 16; ++kk)
-              ptx::mma_ss(tbase + buf * 128, dQk + kmaj(kk), dKVk + 2 * stage * kTile + kmaj(kk), id_qk,
+              ptx::mma_ss(tbase + buf * 128, dQk + kmaj(kk), dKVk + slot(2 * jj) * kTile + kmaj(kk), id_qk,
                           kk > 0);
             ptx::mma_commit(s_full + buf);
           }
           __syncwarp();
         };
-        auto dp_mma = [&](int stage) {   // dP = dO V^T
+        auto dp_mma = [&](int jj) {   // dP = dO V_jj^T; V_jj's last reader
           if (ptx::elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < D / 16; ++kk)
-              ptx::mma_ss(tbase + kDP, dOk + kmaj(kk), dKVk + (2 * stage + 1) * kTile + kmaj(kk), id_qk,
+              ptx::mma_ss(tbase + kDP, dOk + kmaj(kk), dKVk + slot(2 * jj + 1) * kTile + kmaj(kk), id_qk,
                           kk > 0);
             ptx::mma_commit(dp_full);
+            ptx::mma_commit(kv_empty + slot(2 * jj + 1));
           }
           __syncwarp();
         };
-        auto dq_mma = [&](int buf, int stage, bool acc) {   // dQ += dS K (A = dS from TMEM)
+        auto dq_mma = [&](int buf, int jj) {   // dQ += dS K_jj (A = dS from TMEM); K_jj's last reader
           if (ptx::elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < BN / 16; ++kk)
               ptx::mma_ts(tbase + kDQ, tbase + buf * 128 + (kk < 4 ? kk * 8 : 32 + kk * 8),
-                          dKVm + 2 * stage * kTile + (uint64_t)(kk * 2048 >> 4), id_dq,
-                          (acc || kk > 0) ? 1u : 0u);
+                          dKVm + slot(2 * jj) * kTile + (uint64_t)(kk * 2048 >> 4), id_dq,
+                          (jj > 0 || kk > 0) ? 1u : 0u);
             ptx::mma_commit(s_free + buf);
-            ptx::mma_commit(kv_empty + stage);
+            ptx::mma_commit(kv_empty + slot(2 * jj));
           }
           __syncwarp();
         };
         ptx::mbar_wait(q_full, 0);
-        ptx::mbar_wait(kv_full + 0, 0);
+        wait_item(0);
         ptx::tc_fence_after();
         s_mma(0, 0);
+        wait_item(1);
+        ptx::tc_fence_after();
         dp_mma(0);
         for (int u = first, jj = 0; u < nkv; ++jj) {
           const int un = next_live(u + 1);
-          const int buf = jj & 1, stage = jj % C::kStages;
+          const int buf = jj & 1;
           if (un < nkv) {
-            const int sn = (jj + 1) % C::kStages;
-            ptx::mbar_wait(kv_full + sn, ((jj + 1) / C::kStages) & 1);
+            wait_item(2 * jj + 2);
             if (jj >= 1) ptx::mbar_wait(s_free + (buf ^ 1), ((jj - 1) >> 1) & 1);
             ptx::tc_fence_after();
-            s_mma(buf ^ 1, sn);
+            s_mma(buf ^ 1, jj + 1);
             ptx::mbar_wait(dp_free, jj & 1);
+            wait_item(2 * jj + 3);
             ptx::tc_fence_after();
-            dp_mma(sn);
+            dp_mma(jj + 1);
           }
           ptx::mbar_wait(ds_full + buf, (jj >> 1) & 1);
           ptx::tc_fence_after();
-          dq_mma(buf, stage, jj > 0);
+          dq_mma(buf, jj);
           u = un;
         }
         if (ptx::elect_one()) ptx::mma_commit(dq_done);
