@@ -286,31 +286,42 @@ __global__ void __launch_bounds__(kThreads, 1) lao_dq_kernel(const __grid_consta
       if (kGrid && hp.grid_skip && nv > 0) gk = grid_key_bits(hp, qpos, hp.k_begin + k0, nv);
       ptx::mbar_wait(s_full + buf, (jj >> 1) & 1);
       ptx::tc_fence_after();
-      uint32_t r[64], d[64];
-      ptx::tmem_ld32(tbase + lane_off + buf * 128 + 64 * hk, *reinterpret_cast<uint32_t(*)[32]>(r));
-      ptx::tmem_ld32(tbase + lane_off + buf * 128 + 64 * hk + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+      // P from S while dP_jj is still being computed, then dS once dP_jj is in registers
+      const bool full = __all_sync(0xffffffffu, nv == 64 && gk == 0);
+      float pr[64];
+      {
+        uint32_t r[64];
+        ptx::tmem_ld32(tbase + lane_off + buf * 128 + 64 * hk, *reinterpret_cast<uint32_t(*)[32]>(r));
+        ptx::tmem_ld32(tbase + lane_off + buf * 128 + 64 * hk + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+        ptx::tmem_wait_ld();
+        ptx::reg_fence(r);
+#pragma unroll
+        for (int c = 0; c < 64; c += 2) {
+          const float2 x = ptx::ffma2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])),
+                                      make_float2(c2, c2), make_float2(-lse2, -lse2));
+          pr[c] = ptx::ex2(x.x);
+          pr[c + 1] = ptx::ex2(x.y);
+        }
+      }
+      if (!full) {
+#pragma unroll
+        for (int c = 0; c < 64; ++c)
+          if (c >= nv || ((gk >> c) & 1)) pr[c] = 0.f;
+      }
       ptx::mbar_wait(dp_full, jj & 1);
       ptx::tc_fence_after();
+      uint32_t d[64];
       ptx::tmem_ld32(tbase + lane_off + kDP + 64 * hk, *reinterpret_cast<uint32_t(*)[32]>(d));
       ptx::tmem_ld32(tbase + lane_off + kDP + 64 * hk + 32, *reinterpret_cast<uint32_t(*)[32]>(d + 32));
       ptx::tmem_wait_ld();
-      ptx::reg_fence(r);
       ptx::reg_fence(d);
       ptx::tc_fence_before();
       ptx::mbar_arrive(dp_free);   // dP_{jj+1} may overwrite the dP columns
-      const bool full = __all_sync(0xffffffffu, nv == 64 && gk == 0);
       uint32_t pk[32];
 #pragma unroll
       for (int c = 0; c < 64; c += 2) {
-        const float2 x = ptx::ffma2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])),
-                                    make_float2(c2, c2), make_float2(-lse2, -lse2));
-        float p0 = ptx::ex2(x.x), p1 = ptx::ex2(x.y);
-        if (!full) {
-          if (c >= nv || ((gk >> c) & 1)) p0 = 0.f;
-          if (c + 1 >= nv || ((gk >> (c + 1)) & 1)) p1 = 0.f;
-        }
         // dS = P * (dP - D)
-        const float2 ds = ptx::fmul2(make_float2(p0, p1),
+        const float2 ds = ptx::fmul2(make_float2(pr[c], pr[c + 1]),
                                      ptx::fadd2(make_float2(__uint_as_float(d[c]), __uint_as_float(d[c + 1])),
                                                 make_float2(-Dv, -Dv)));
         pk[c >> 1] = ptx::pack_bf16(ds.x, ds.y);
