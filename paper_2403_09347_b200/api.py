@@ -111,9 +111,10 @@ def burst_attn_func(q, k, v, causal: bool = False, softmax_scale: float | None =
     communicator is aborted and the pass raises DeadlockError (default
     BURST_RING_TIMEOUT_S or 600; the reference's deadlock_timeout, sim.py:501-510).
     Every exchange also carries a small header checked at pass end (RingDesyncError).
-    `deterministic`: reduce every dQ tile in ascending key-tile order so gradients are
-    bit-reproducible run to run and across transports (the reference's bitwise
-    executor equivalence, pkg/tests/test_sim.py:280-295); slower backward.
+    `deterministic`: dQ from a query-stationary kernel that sums each row over the key
+    tiles in order (one writer per row) so gradients are bit-reproducible run to run
+    and across transports (the reference's bitwise executor equivalence,
+    pkg/tests/test_sim.py:280-295); ~1/3 slower backward.
     `start_offset`: rank r starts the ring with the K/V block of rank r - start_offset
     (mod G) instead of its own (initial_forward_body, ring.py:137-143); one extra
     exchange, the merge order rotates and values agree to rounding.

@@ -90,8 +90,8 @@ def local_backward(q, k, v, dout, o, lse, softmax_scale: float | None = None,
     """Gradient contributions (dQ, dK, dV) of one rectangle (local_attn.py:255-289).
 
     `o`, `lse`: this block's forward outputs (D = rowsum(dO * O) is formed on the
-    device, ring.init_backward ring.py:195-218).  `deterministic`: ordered dQ
-    reductions (bit-reproducible)."""
+    device, ring.init_backward ring.py:195-218).  `deterministic`: dQ from the
+    query-stationary kernel (one writer per row: bit-reproducible)."""
     check_qkv(q, k, v)
     if dout.shape != q.shape or o.shape != q.shape:
         raise ShapeError(f"dO and O must be {tuple(q.shape)}")
