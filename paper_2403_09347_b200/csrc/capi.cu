@@ -261,6 +261,7 @@ int launch_fwd_f32(const burst_hop* h, const void* q, const void* k, const void*
 template <int D>
 int launch_dq_bf16(const burst_hop* h, const void* q, const void* k, const void* v, const void* dout,
                    const float* stats, float* dq_acc, cudaStream_t st) {
+  if (h->q_len <= 0) return BURST_OK;   // no query rows: no dQ contribution
   bdq::Params p;
   memset(&p, 0, sizeof(p));
   int rc;
